@@ -1,0 +1,130 @@
+// Host side of the tcgen05 GEMM: TMA descriptors, tiling, split-K, launch.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "../../include/fade_b200.h"
+#include "gemm.cuh"
+
+namespace fade {
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encoder() {
+  static std::once_flag once;
+  static int status = FADE_OK;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr) {
+      set_last_error("cuTensorMapEncodeTiled unavailable from the driver");
+      status = FADE_ERR_CUDA;
+      return;
+    }
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  });
+  return status;
+}
+
+static int encode(CUtensorMap* map, const float* ptr, long long inner, long long outer,
+                  long long ld, int box_inner, int box_outer, CUtensorMapSwizzle swz) {
+  if (int s = get_encoder()) return s;
+  if (((uintptr_t)ptr & 15) || (ld * 4) % 16) {
+    set_last_error("TMA operand must be 16-byte aligned with a 16-byte multiple row pitch");
+    return FADE_ERR_USAGE;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char b[160];
+    snprintf(b, sizeof(b), "cuTensorMapEncodeTiled failed (%d) inner=%lld outer=%lld ld=%lld", (int)r,
+             inner, outer, ld);
+    set_last_error(b);
+    return FADE_ERR_CUDA;
+  }
+  return FADE_OK;
+}
+
+// K-major operand: logical [mn][k] rows of K; box = 32 K x box_mn rows
+int make_tmap_kmajor(CUtensorMap* map, const float* ptr, long long mn, long long k, long long ld,
+                     int box_mn) {
+  return encode(map, ptr, k, mn, ld, kBK, box_mn, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+// MN-major operand: logical [k][mn] rows of MN; box = 32 MN x BK rows of K
+int make_tmap_mnmajor(CUtensorMap* map, const float* ptr, long long mn, long long k, long long ld) {
+  return encode(map, ptr, mn, k, ld, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
+int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
+  memset(P, 0, sizeof(*P));
+  P->M = d.M;
+  P->N = d.N;
+  P->K = d.K;
+  // A: a_trans == 0 -> A[m*lda + k] (K-major); 1 -> A[k*lda + m] (M-major)
+  P->a_mn = d.a_trans;
+  // B: b_trans == 0 -> B[k*ldb + n] (N-major); 1 -> B[n*ldb + k] (K-major)
+  P->b_mn = d.b_trans ? 0 : 1;
+  int s;
+  if (!P->a_mn) s = make_tmap_kmajor(&P->ta, d.A, d.M, d.K, d.lda, kBM);
+  else s = make_tmap_mnmajor(&P->ta, d.A, d.M, d.K, d.lda);
+  if (s) return s;
+  if (!P->b_mn) s = make_tmap_kmajor(&P->tb, d.B, d.N, d.K, d.ldb, BN);
+  else s = make_tmap_mnmajor(&P->tb, d.B, d.N, d.K, d.ldb);
+  if (s) return s;
+  const int kt = cdiv(d.K, kBK);
+  const int splits = std::max(1, std::min(d.splits, kt));
+  P->k_tiles_per_split = cdiv(kt, splits);
+  P->splits = cdiv(kt, P->k_tiles_per_split);   // no empty split
+  P->tiles_m = cdiv(d.M, kBM);
+  P->tiles_n = cdiv(d.N, BN);
+  P->epi = d.epi;
+  P->C = d.C;
+  P->ldc = d.ldc;
+  P->c_split = d.c_split;
+  P->bias = d.bias;
+  P->aux0 = d.aux0;
+  P->aux1 = d.aux1;
+  P->aux2 = d.aux2;
+  P->ld_aux = d.ld_aux;
+  if (P->splits > 1 && d.epi != EPI_STORE) {
+    set_last_error("split-K is only valid with the partial-store epilogue");
+    return FADE_ERR_USAGE;
+  }
+  return FADE_OK;
+}
+
+template <int BN>
+static int launch_bn(GemmParams& G, cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+  });
+  FADE_CUDA_TRY(attr_err);
+  k_gemm_tf32<BN><<<G.total_tiles, kGemmThreads, Cfg::kSmem, st>>>(G);
+  FADE_CUDA_TRY(cudaGetLastError());
+  return FADE_OK;
+}
+
+int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
+  int t = 0;
+  for (int q = 0; q < G.nprob; ++q) {
+    G.prob[q].tile_begin = t;
+    t += G.prob[q].tiles_m * G.prob[q].tiles_n * G.prob[q].splits;
+  }
+  G.total_tiles = t;
+  if (t == 0) return FADE_OK;
+  if (BN == 64) return launch_bn<64>(G, st);
+  if (BN == 128) return launch_bn<128>(G, st);
+  set_last_error("unsupported GEMM tile width");
+  return FADE_ERR_USAGE;
+}
+
+}  // namespace fade

@@ -1,0 +1,51 @@
+"""tcgen05 TF32 GEMM vs a plain torch fp32/fp64 reference (all operand majors,
+split-K, ragged edges)."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def run(M, N, K, a_trans, b_trans, splits=1, bn=128):
+    from paper_2604_07239_b200 import _native
+    lib = _native.lib()
+    g = torch.Generator(device="cuda").manual_seed(M * 131 + N * 7 + K)
+    A = torch.randn(M, K, device="cuda", generator=g)
+    B = torch.randn(K, N, device="cuda", generator=g)
+    As = A.t().contiguous() if a_trans else A.contiguous()       # [K][M] or [M][K]
+    Bs = B.t().contiguous() if b_trans else B.contiguous()       # [N][K] or [K][N]
+    ldc = (N + 3) // 4 * 4
+    C = torch.full((splits, M, ldc), float("nan"), device="cuda")
+    st = lib.fade_debug_gemm(As.data_ptr(), As.shape[1], a_trans, Bs.data_ptr(), Bs.shape[1],
+                             b_trans, C.data_ptr(), ldc, M, N, K, splits, bn, None)
+    assert st == 0, _native.last_error()
+    torch.cuda.synchronize()
+    ref = (A.double() @ B.double())
+    kt = (K + 31) // 32
+    per = -(-kt // max(1, min(splits, kt)))
+    used = -(-kt // per)
+    got = C[:used, :, :N].double().sum(0)
+    err = (got - ref).abs().max().item() / max(1e-9, ref.abs().max().item())
+    return err
+
+
+@pytest.mark.parametrize("a_trans,b_trans", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("bn", [64, 128])
+def test_majors(a_trans, b_trans, bn):
+    assert run(256, 256, 512, a_trans, b_trans, bn=bn) < 3e-3
+
+
+@pytest.mark.parametrize("shape", [(512, 512, 4096), (100, 72, 40), (16, 40, 32), (512, 16384, 512),
+                                   (4096, 512, 512), (130, 260, 200)])
+def test_shapes(shape):
+    M, N, K = shape
+    assert run(M, N, K, 0, 0) < 3e-3
+    if M % 4 == 0:     # an M-major A needs a 16-byte row pitch
+        assert run(M, N, K, 1, 0, bn=64) < 3e-3
+
+
+@pytest.mark.parametrize("splits", [2, 4, 8])
+def test_split_k(splits):
+    assert run(512, 512, 8192, 0, 0, splits=splits, bn=64) < 3e-3

@@ -66,8 +66,8 @@ struct DecLane {
 
 // kernels.py:200-233 for one stream.  cum: 257 ascending entries.
 // Returns 0 ok, 1 invalid code, 2 truncated; sym receives the symbol.
-template <typename CumT>
-__device__ __forceinline__ int dec_symbol(DecLane& s, const CumT* cum, const uint8_t* data,
+template <typename CumT>   // CumT: pointer/array of 257 entries or an indexable functor
+__device__ __forceinline__ int dec_symbol(DecLane& s, const CumT& cum, const uint8_t* data,
                                           int64_t dlen, int* sym) {
   const uint64_t r = s.rng >> 16;
   const uint64_t dv = s.code / r;

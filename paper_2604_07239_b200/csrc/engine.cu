@@ -1,0 +1,1067 @@
+// The FADE step engine: device state, the per-timestep kernel schedule
+// (model stream + weight-gradient side stream + CSPP coder stream), CUDA-graph
+// replay, and the C ABI of include/fade_b200.h sections 2-3.
+//
+// One timestep (pipeline.py:211-223 serial order, 251-287 pipelined):
+//   forward  : trunk -> {route, mem} GEMMs -> mix -> down GEMM -> bmm ->
+//              {up, cgate} GEMMs -> coarse -> e12 GEMM (GeGLU epilogue) ->
+//              f GEMM (split-K) -> out -> head GEMM -> head (softmax, quantise,
+//              cum slot, [decode], xent)
+//   coder    : encode(cum slot) on its own stream, overlapping the backward
+//   backward : dX GEMMs + row kernels on the model stream; every dW GEMM (with
+//              Adam fused in its epilogue) on a side stream as soon as its
+//              input gradient exists and the dX GEMM that reads the old weight
+//              is done; small parameters and the embedding last.
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/fade_b200.h"
+#include "model.cuh"
+#include "stream_coder.cuh"
+
+namespace fade {
+
+#define TRY(expr)                    \
+  do {                               \
+    int _s = (expr);                 \
+    if (_s != FADE_OK) return _s;    \
+  } while (0)
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return FADE_OK;
+  set_last_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return FADE_ERR_CUDA;
+}
+#define CK(expr) TRY(cuda_fail((expr), #expr))
+
+static size_t align_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
+
+struct DevArena {            // one cudaMalloc carved into 256-byte aligned pieces
+  char* base = nullptr;
+  size_t used = 0, cap = 0;
+  std::vector<std::pair<size_t, size_t>> pending;
+  size_t reserve(size_t bytes) {
+    const size_t off = align_up(used, 256);
+    used = off + bytes;
+    return off;
+  }
+};
+
+enum GemmId {
+  G_ROUTE_MEM, G_DOWN, G_UP_CGATE, G_E12, G_F, G_HEAD,          // forward
+  G_DH, G_DWIDE, G_DZ2, G_DU_DHMC, G_DZ, G_DXR_DBLOCK,          // input gradients
+  G_WHEAD, G_WF, G_W12, G_WUP_WCGATE, G_WDOWN, G_WROUTE_WMEM,   // weight gradients + Adam
+  G_COUNT
+};
+
+}  // namespace fade
+
+using namespace fade;
+
+struct fade_model {
+  fade_config_t cfg;
+  Dims d;
+  SmallLayout sl;
+  int device = 0;
+  cudaStream_t s_main = nullptr, s_side = nullptr, s_coder = nullptr;
+  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_cum[2] = {}, ev_enc[2] = {}, ev_side_done = nullptr, ev_coder_join = nullptr;
+  void* mem = nullptr;
+  ModelPtrs M;
+  StepState* st = nullptr;      // device
+  GemmParams G[G_COUNT];
+  int bn[G_COUNT];
+  uint8_t* ctx_buf = nullptr;   // [B][T]  (predict API)
+  uint8_t* tgt_buf = nullptr;   // [B]
+  double* loss_buf = nullptr;   // [1]
+  float* cache_snap = nullptr;  // [B][C] for state-free test hooks
+  float* w12_g = nullptr;
+  bool live = false;            // a predict is pending train_step
+  int launches_per_step = 0;
+};
+
+struct fade_coder {
+  int B = 0;
+  long long L = 0, cap = 0;
+  void* mem = nullptr;
+  EncState e;
+  std::vector<long long> lengths;
+  cudaStream_t s = nullptr;
+};
+
+namespace fade {
+
+// ---------------------------------------------------------------------------
+// allocation
+
+static SmallLayout make_small_layout(const Dims& d) {
+  SmallLayout s;
+  int o = 0;
+  s.out_g = o; o += d.H;  s.out_b = o; o += d.H;
+  s.ref_g = o; o += d.H;  s.ref_b = o; o += d.H;
+  s.mix_g = o; o += d.H;  s.mix_b = o; o += d.H;
+  s.in_g = o;  o += d.H;  s.in_b = o;  o += d.H;
+  s.loc_g = o; o += d.D;  s.loc_b = o; o += d.D;  s.conv_b = o; o += d.D;
+  s.conv_k = o; o += d.K * d.D * d.D;
+  s.w_gate = o; o += d.D * d.D;  s.w_val = o; o += d.D * d.D;
+  s.lam_out = o++; s.lam_mix = o++; s.lam_mem = o++;
+  s.rowred = o;
+  s.b_head = o; o += 256;
+  s.total = o;
+  return s;
+}
+
+// element count of parameter i in the reference layout
+static long long ref_numel(const Dims& d, int i) {
+  switch (i) {
+    case P_EMB: return 256LL * d.D;
+    case P_IN_LN_G: case P_IN_LN_B: case P_MIX_LN_G: case P_MIX_LN_B: case P_REF_LN_G:
+    case P_REF_LN_B: case P_OUT_LN_G: case P_OUT_LN_B: return d.H;
+    case P_W_GATE: case P_W_VAL: return (long long)d.D * d.D;
+    case P_W_MEM: return (long long)d.C * d.H;
+    case P_LAM_MEM: case P_LAM_MIX: case P_LAM_OUT: return 1;
+    case P_LOC_LN_G: case P_LOC_LN_B: case P_CONV_B: return d.D;
+    case P_CONV_K: return (long long)d.K * d.D * d.D;
+    case P_W_ROUTE: case P_W_CGATE: return (long long)d.H * d.H;
+    case P_W_DOWN: case P_W_UP: return (long long)d.H * d.X;
+    case P_W_MIX: return (long long)d.B * d.X * d.X;
+    case P_W_E1: case P_W_E2: return (long long)d.H * d.E;
+    case P_W_F: return (long long)d.E * d.H;
+    case P_W_HEAD: return (long long)d.H * 256;
+    case P_B_HEAD: return 256;
+  }
+  return 0;
+}
+
+static int small_offset(const SmallLayout& s, int i) {
+  switch (i) {
+    case P_OUT_LN_G: return s.out_g;  case P_OUT_LN_B: return s.out_b;
+    case P_REF_LN_G: return s.ref_g;  case P_REF_LN_B: return s.ref_b;
+    case P_MIX_LN_G: return s.mix_g;  case P_MIX_LN_B: return s.mix_b;
+    case P_IN_LN_G: return s.in_g;    case P_IN_LN_B: return s.in_b;
+    case P_LOC_LN_G: return s.loc_g;  case P_LOC_LN_B: return s.loc_b;
+    case P_CONV_B: return s.conv_b;   case P_CONV_K: return s.conv_k;
+    case P_W_GATE: return s.w_gate;   case P_W_VAL: return s.w_val;
+    case P_LAM_OUT: return s.lam_out; case P_LAM_MIX: return s.lam_mix;
+    case P_LAM_MEM: return s.lam_mem; case P_B_HEAD: return s.b_head;
+  }
+  return -1;
+}
+
+static int choose_splits(int tiles, int k_tiles) {
+  int s = (148 + tiles - 1) / tiles;
+  s = std::max(1, std::min(s, k_tiles / 4));
+  return s;
+}
+
+struct Builder {
+  GemmParams* G;
+  int BN;
+  int add(const GemmDesc& d) {
+    if (G->nprob >= kMaxProblems) {
+      set_last_error("too many GEMM problems in one group");
+      return FADE_ERR_USAGE;
+    }
+    return gemm_setup(&G->prob[G->nprob++], d, BN);
+  }
+};
+
+static GemmDesc gd(const float* A, long long lda, int at, const float* B, long long ldb, int bt,
+                   int M, int N, int K, int epi, float* C, long long ldc) {
+  GemmDesc g{};
+  g.A = A; g.lda = lda; g.a_trans = at;
+  g.B = B; g.ldb = ldb; g.b_trans = bt;
+  g.M = M; g.N = N; g.K = K;
+  g.splits = 1;
+  g.epi = epi;
+  g.C = C; g.ldc = ldc;
+  return g;
+}
+
+static int build_gemms(fade_model* m) {
+  const Dims& d = m->d;
+  ModelPtrs& M = m->M;
+  Acts& a = M.a;
+  const int B = d.B, H = d.H, X = d.X, E = d.E, Ep = d.Ep, C = d.C;
+  for (int i = 0; i < G_COUNT; ++i) {
+    memset(&m->G[i], 0, sizeof(GemmParams));
+    m->bn[i] = 64;
+    m->G[i].adam = &m->st->adam;
+  }
+  m->bn[G_E12] = 128;
+  auto b = [&](int id) { return Builder{&m->G[id], m->bn[id]}; };
+  Tensor4* w = M.w;
+  // forward
+  {
+    auto bl = b(G_ROUTE_MEM);
+    TRY(bl.add(gd(a.x, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, a.rpre, H)));
+    GemmDesc g = gd(a.cache, C, 0, w[P_W_MEM].p, H, 0, B, H, C, EPI_STORE, a.ws_mem, H);
+    g.splits = M.splits_mem;
+    g.c_split = (long long)B * H;
+    TRY(bl.add(g));
+  }
+  TRY(b(G_DOWN).add(gd(a.z, H, 0, w[P_W_DOWN].p, X, 0, B, X, H, EPI_STORE, a.zd, X)));
+  {
+    auto bl = b(G_UP_CGATE);
+    TRY(bl.add(gd(a.u, X, 0, w[P_W_UP].p, H, 0, B, H, X, EPI_STORE, a.inner, H)));
+    TRY(bl.add(gd(a.h_mix, H, 0, w[P_W_CGATE].p, H, 0, B, H, H, EPI_STORE, a.cpre, H)));
+  }
+  {
+    GemmDesc g = gd(a.z2, H, 0, w[P_W_E1].p, 2LL * Ep, 0, B, 2 * Ep, H, EPI_GEGLU, a.a12, 2LL * Ep);
+    g.aux0 = a.wide;
+    g.ld_aux = Ep;
+    TRY(b(G_E12).add(g));
+  }
+  {
+    GemmDesc g = gd(a.wide, Ep, 0, w[P_W_F].p, H, 0, B, H, E, EPI_STORE, a.ws_f, H);
+    g.splits = M.splits_f;
+    g.c_split = (long long)B * H;
+    TRY(b(G_F).add(g));
+  }
+  {
+    GemmDesc g = gd(a.h, H, 0, w[P_W_HEAD].p, 256, 0, B, 256, H, EPI_STORE, a.logits, 256);
+    g.bias = w[P_B_HEAD].p;
+    TRY(b(G_HEAD).add(g));
+  }
+  // input gradients
+  TRY(b(G_DH).add(gd(a.dlogits, 256, 0, w[P_W_HEAD].p, 256, 1, B, H, 256, EPI_STORE, a.dh, H)));
+  {
+    GemmDesc g = gd(a.dnpre, H, 0, w[P_W_F].p, H, 1, B, E, H, EPI_GEGLU_BWD, a.da12, 2LL * Ep);
+    g.aux1 = a.a12;
+    g.ld_aux = 2LL * Ep;
+    // W_f has E rows; rows [E, Ep) read as zeros through the TMA bounds, and the
+    // tiles cover whole 64-column interleave blocks of dA12
+    TRY(b(G_DWIDE).add(g));
+    m->G[G_DWIDE].prob[0].N = Ep;
+    m->G[G_DWIDE].prob[0].tiles_n = cdiv(Ep, 64);
+  }
+  {
+    GemmDesc g = gd(a.da12, 2LL * Ep, 0, w[P_W_E1].p, 2LL * Ep, 1, B, H, 2 * Ep, EPI_STORE, a.ws_dz2, H);
+    g.splits = M.splits_dz2;
+    g.c_split = (long long)B * H;
+    TRY(b(G_DZ2).add(g));
+  }
+  {
+    auto bl = b(G_DU_DHMC);
+    TRY(bl.add(gd(a.dinner, H, 0, w[P_W_UP].p, H, 1, B, X, H, EPI_STORE, a.du, X)));
+    TRY(bl.add(gd(a.dcpre, H, 0, w[P_W_CGATE].p, H, 1, B, H, H, EPI_STORE, a.dhm_c, H)));
+  }
+  TRY(b(G_DZ).add(gd(a.dzd, X, 0, w[P_W_DOWN].p, X, 1, B, H, X, EPI_STORE, a.dz, H)));
+  {
+    auto bl = b(G_DXR_DBLOCK);
+    TRY(bl.add(gd(a.drpre, H, 0, w[P_W_ROUTE].p, H, 1, B, H, H, EPI_STORE, a.dx_r, H)));
+    TRY(bl.add(gd(a.dupre, H, 0, w[P_W_MEM].p + (long long)(C - d.D) * H, H, 1, B, d.D, H,
+                  EPI_STORE, a.dblock, d.D)));
+  }
+  // weight gradients with the Adam step fused into the epilogue
+  auto adam = [&](GemmDesc g, const Tensor4& t) {
+    g.C = t.p;
+    g.aux0 = t.m;
+    g.aux2 = t.v;
+    return g;
+  };
+  TRY(b(G_WHEAD).add(adam(gd(a.h, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD])));
+  TRY(b(G_WF).add(adam(gd(a.wide, Ep, 1, a.dnpre, H, 0, E, H, B, EPI_ADAM, nullptr, H), w[P_W_F])));
+  TRY(b(G_W12).add(adam(gd(a.z2, H, 1, a.da12, 2LL * Ep, 0, H, 2 * Ep, B, EPI_ADAM, nullptr, 2LL * Ep), w[P_W_E1])));
+  {
+    auto bl = b(G_WUP_WCGATE);
+    TRY(bl.add(adam(gd(a.u, X, 1, a.dinner, H, 0, X, H, B, EPI_ADAM, nullptr, H), w[P_W_UP])));
+    TRY(bl.add(adam(gd(a.h_mix, H, 1, a.dcpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_CGATE])));
+  }
+  TRY(b(G_WDOWN).add(adam(gd(a.z, H, 1, a.dzd, X, 0, H, X, B, EPI_ADAM, nullptr, X), w[P_W_DOWN])));
+  {
+    auto bl = b(G_WROUTE_WMEM);
+    TRY(bl.add(adam(gd(a.x, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE])));
+    TRY(bl.add(adam(gd(a.cache, C, 1, a.dupre, H, 0, C, H, B, EPI_ADAM, nullptr, H), w[P_W_MEM])));
+  }
+  return FADE_OK;
+}
+
+static int run_gemm(fade_model* m, int id, cudaStream_t s, bool grad_only = false) {
+  GemmParams G = m->G[id];
+  if (grad_only) {
+    for (int q = 0; q < G.nprob; ++q) {
+      GemmProblem& P = G.prob[q];
+      if (P.epi != EPI_ADAM) continue;
+      // the gradient buffer sits at the same offset in the g arena as C in p
+      for (int i = 0; i < P_COUNT; ++i)
+        if (m->M.w[i].p == P.C) {
+          P.C = m->M.w[i].g;
+          break;
+        }
+      P.epi = EPI_GRAD;
+    }
+  }
+  return gemm_launch(G, m->bn[id], s);
+}
+
+static int allocate(fade_model* m) {
+  const Dims& d = m->d;
+  const long long B = d.B, H = d.H, X = d.X, Ep = d.Ep, C = d.C;
+  ModelPtrs& M = m->M;
+  memset(&M, 0, sizeof(M));
+  M.d = d;
+  M.sl = m->sl;
+  // split-K factors sized to ~one wave of 148 SMs (BN = 64 tiles)
+  const int tiles = cdiv(B, kBM) * cdiv(H, 64);
+  M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
+  M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
+  M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
+  M.emb_chunk = 16;
+
+  struct Item { void** ptr; size_t bytes; };
+  std::vector<Item> items;
+  auto F = [&](float** p, long long n) { items.push_back({(void**)p, sizeof(float) * (size_t)n}); };
+  // parameters: big tensors get p/m/v/g; small ones live in the small arena
+  float* big[P_COUNT][4] = {};
+  for (int i = 0; i < P_COUNT; ++i) {
+    if (small_offset(m->sl, i) >= 0 || i == P_W_E2) continue;
+    long long n = ref_numel(d, i);
+    if (i == P_W_E1) n = H * 2 * Ep;   // interleaved W12
+    for (int k = 0; k < 4; ++k) F(&big[i][k], n);
+  }
+  float *sp, *smm, *sv, *sg;
+  F(&sp, m->sl.total); F(&smm, m->sl.total); F(&sv, m->sl.total); F(&sg, m->sl.total);
+  Acts& a = M.a;
+  F(&a.x, B * H); F(&a.x_hat, B * H); F(&a.x_inv, B); F(&a.gpre, B * d.D); F(&a.vpre, B * d.D);
+  F(&a.loc, B * H); F(&a.loc_hat, B * H); F(&a.loc_inv, B * d.T); F(&a.conv_pre, B * H);
+  F(&a.h_l, B * H); F(&a.cache, B * C); F(&a.rpre, B * H);
+  F(&a.ws_mem, (long long)M.splits_mem * B * H); F(&a.upre, B * H); F(&a.h_g, B * H);
+  F(&a.alpha, B * H); F(&a.h_mix, B * H); F(&a.z_hat, B * H); F(&a.z_inv, B); F(&a.z, B * H);
+  F(&a.zd, B * X); F(&a.u, B * X); F(&a.inner, B * H); F(&a.cpre, B * H); F(&a.gate, B * H);
+  F(&a.h_c, B * H); F(&a.z2_hat, B * H); F(&a.z2_inv, B); F(&a.z2, B * H);
+  F(&a.a12, B * 2 * Ep); F(&a.wide, B * Ep); F(&a.ws_f, (long long)M.splits_f * B * H);
+  F(&a.n_hat, B * H); F(&a.n_inv, B); F(&a.nrm, B * H); F(&a.h, B * H); F(&a.logits, B * 256);
+  items.push_back({(void**)&a.probs, sizeof(double) * (size_t)B * 256});
+  items.push_back({(void**)&a.cum, sizeof(unsigned) * 2 * (size_t)B * kCumLd});
+  items.push_back({(void**)&a.nll, sizeof(double) * (size_t)B});
+  F(&a.alpha_row, B * 3);
+  F(&a.dlogits, B * 256); F(&a.dh, B * H); F(&a.dhc, B * H); F(&a.dnpre, B * H);
+  F(&a.da12, B * 2 * Ep); F(&a.ws_dz2, (long long)M.splits_dz2 * B * H); F(&a.dinner, B * H);
+  F(&a.dcpre, B * H); F(&a.du, B * X); F(&a.dhm_c, B * H); F(&a.dzd, B * X); F(&a.dz, B * H);
+  F(&a.drpre, B * H); F(&a.dupre, B * H); F(&a.dh_l, B * H); F(&a.dx_part, B * H);
+  F(&a.dx_r, B * H); F(&a.dblock, B * d.D); F(&a.demb, B * H);
+  F(&a.rowred, B * m->sl.rowred);
+  F(&a.emb_part, (long long)cdiv(B, M.emb_chunk) * 256 * d.D);
+  items.push_back({(void**)&m->st, sizeof(StepState)});
+  items.push_back({(void**)&m->ctx_buf, (size_t)B * d.T});
+  items.push_back({(void**)&m->tgt_buf, (size_t)B});
+  items.push_back({(void**)&m->loss_buf, sizeof(double) * 4});
+  F(&m->cache_snap, B * C);
+
+  size_t total = 0;
+  std::vector<size_t> offs;
+  for (auto& it : items) {
+    total = align_up(total, 256);
+    offs.push_back(total);
+    total += it.bytes;
+  }
+  CK(cudaMalloc(&m->mem, total));
+  CK(cudaMemset(m->mem, 0, total));
+  for (size_t k = 0; k < items.size(); ++k) *items[k].ptr = (char*)m->mem + offs[k];
+
+  M.small_p = sp; M.small_m = smm; M.small_v = sv; M.small_g = sg;
+  for (int i = 0; i < P_COUNT; ++i) {
+    const int so = small_offset(m->sl, i);
+    if (so >= 0) {
+      M.w[i] = Tensor4{sp + so, smm + so, sv + so, sg + so};
+    } else {
+      const int src = (i == P_W_E2) ? P_W_E1 : i;   // e1 and e2 share the interleaved W12
+      M.w[i] = Tensor4{big[src][0], big[src][1], big[src][2], big[src][3]};
+    }
+  }
+  M.st = m->st;
+  StepState init{};
+  init.err_key = ~0ull;
+  CK(cudaMemcpy(m->st, &init, sizeof(init), cudaMemcpyHostToDevice));
+  return FADE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the timestep schedule
+
+struct StepIO {
+  const uint8_t* src;        // context source (stream matrix or ctx buffer)
+  long long ld_src;
+  int use_col;               // ctx = src[b, col-T:col] (else src[b, 0:T])
+  HeadArgs head;
+};
+
+static int forward(fade_model* m, const StepIO& io, bool with_head) {
+  cudaStream_t s = m->s_main;
+  const ModelPtrs& M = m->M;
+  launch_trunk_fwd(M, io.src, io.ld_src, io.use_col, s);
+  TRY(run_gemm(m, G_ROUTE_MEM, s));
+  launch_mix_fwd(M, s);
+  TRY(run_gemm(m, G_DOWN, s));
+  launch_bmm_fwd(M, s);
+  TRY(run_gemm(m, G_UP_CGATE, s));
+  launch_coarse_fwd(M, s);
+  TRY(run_gemm(m, G_E12, s));
+  TRY(run_gemm(m, G_F, s));
+  launch_out_fwd(M, s);
+  TRY(run_gemm(m, G_HEAD, s));
+  if (with_head) launch_head(M, io.head, s);
+  CK(cudaGetLastError());
+  return FADE_OK;
+}
+
+// fork the side stream off the model stream at this point
+static int fork_side(fade_model* m, int k) {
+  CK(cudaEventRecord(m->ev[k], m->s_main));
+  CK(cudaStreamWaitEvent(m->s_side, m->ev[k], 0));
+  return FADE_OK;
+}
+
+static int backward(fade_model* m, const StepIO& io, bool grad_only, double* losses) {
+  cudaStream_t s = m->s_main, side = m->s_side;
+  const ModelPtrs& M = m->M;
+  if (!grad_only) launch_adam_prep(M, m->cfg.lr, m->cfg.beta1, m->cfg.beta2, m->cfg.adam_eps, s);
+  TRY(run_gemm(m, G_DH, s));
+  TRY(fork_side(m, 0));
+  TRY(run_gemm(m, G_WHEAD, side, grad_only));
+  launch_out_bwd(M, s);
+  TRY(run_gemm(m, G_DWIDE, s));
+  TRY(fork_side(m, 1));
+  TRY(run_gemm(m, G_WF, side, grad_only));
+  TRY(run_gemm(m, G_DZ2, s));
+  TRY(fork_side(m, 2));
+  TRY(run_gemm(m, G_W12, side, grad_only));
+  launch_coarse_bwd(M, s);
+  TRY(run_gemm(m, G_DU_DHMC, s));
+  TRY(fork_side(m, 3));
+  TRY(run_gemm(m, G_WUP_WCGATE, side, grad_only));
+  launch_bmm_bwd(M, grad_only, s);
+  TRY(run_gemm(m, G_DZ, s));
+  TRY(fork_side(m, 4));
+  TRY(run_gemm(m, G_WDOWN, side, grad_only));
+  launch_mix_bwd(M, s);
+  TRY(run_gemm(m, G_DXR_DBLOCK, s));
+  TRY(fork_side(m, 5));
+  TRY(run_gemm(m, G_WROUTE_WMEM, side, grad_only));
+  launch_trunk_bwd(M, io.src, io.ld_src, io.use_col, s);
+  launch_small_adam(M, grad_only, losses, s);
+  launch_emb_grad(M, io.src, io.ld_src, io.use_col, grad_only, s);
+  CK(cudaEventRecord(m->ev_side_done, side));
+  CK(cudaStreamWaitEvent(s, m->ev_side_done, 0));
+  CK(cudaGetLastError());
+  return FADE_OK;
+}
+
+static int check_error(fade_model* m, fade_error_t* err) {
+  unsigned long long key = 0;
+  CK(cudaMemcpy(&key, &m->st->err_key, sizeof(key), cudaMemcpyDeviceToHost));
+  if (key == ~0ull) return FADE_OK;
+  const int code = (int)(key & 7);
+  const long long stream = (long long)((key >> 3) & ((1ull << 21) - 1));
+  const long long step = (long long)(key >> 24);
+  int kind = FADE_ERR_CORRUPT, why = 0;
+  const char* msg = "";
+  switch (code) {
+    case 1: kind = FADE_ERR_CORRUPT; why = 1; msg = "invalid code value"; break;
+    case 2: kind = FADE_ERR_CORRUPT; why = 2; msg = "truncated stream"; break;
+    case 3: kind = FADE_ERR_DIVERGED; msg = "non-finite value in forward output"; break;
+    case 4: kind = FADE_ERR_QUANT; msg = "row does not sum to 1 within quantizer tolerance"; break;
+    case 5: kind = FADE_ERR_DIVERGED; msg = "non-finite loss"; break;
+    case 6: kind = FADE_ERR_CORRUPT; why = 2; msg = "stream shorter than coder tail"; break;
+  }
+  if (err) {
+    err->kind = kind;
+    err->why = why;
+    err->stream = stream;
+    err->step = code == 6 ? -1 : step;
+  }
+  set_last_error(msg);
+  // reset so the model object stays usable after the caller handles the error
+  unsigned long long none = ~0ull;
+  CK(cudaMemcpy(&m->st->err_key, &none, sizeof(none), cudaMemcpyHostToDevice));
+  return kind;
+}
+
+static int set_col(fade_model* m, long long col, long long loss_base) {
+  long long v[2] = {col, 0};
+  CK(cudaMemcpyAsync(&m->st->col, &col, sizeof(long long), cudaMemcpyHostToDevice, m->s_main));
+  v[1] = loss_base;
+  CK(cudaMemcpyAsync(&m->st->loss_base, &v[1], sizeof(long long), cudaMemcpyHostToDevice, m->s_main));
+  CK(cudaStreamSynchronize(m->s_main));
+  return FADE_OK;
+}
+
+}  // namespace fade
+
+// ===========================================================================
+// C ABI
+extern "C" {
+
+int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) {
+  *out = nullptr;
+  if (cfg->alphabet != 256 || cfg->embed_dim % 4 || cfg->mix_dim % 4 || cfg->expand_dim % 4 ||
+      cfg->cache_dim % cfg->embed_dim || cfg->conv_kernel % 2 == 0 || cfg->batch < 1 ||
+      cfg->ctx_len < 1) {
+    set_last_error("unsupported model geometry for the B200 kernels");
+    return FADE_ERR_USAGE;
+  }
+  std::unique_ptr<fade_model> m(new fade_model());
+  m->cfg = *cfg;
+  m->device = device;
+  Dims& d = m->d;
+  d.B = cfg->batch;
+  d.T = cfg->ctx_len;
+  d.D = cfg->embed_dim;
+  d.H = cfg->ctx_len * cfg->embed_dim;
+  d.C = cfg->cache_dim;
+  d.X = cfg->mix_dim;
+  d.E = cfg->expand_dim;
+  d.Ep = (cfg->expand_dim + 63) / 64 * 64;
+  d.K = cfg->conv_kernel;
+  m->sl = make_small_layout(d);
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&m->s_main, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&m->s_side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&m->s_coder, cudaStreamNonBlocking));
+  for (auto& e : m->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaEventCreateWithFlags(&m->ev_cum[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&m->ev_enc[i], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&m->ev_side_done, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&m->ev_coder_join, cudaEventDisableTiming));
+  TRY(allocate(m.get()));
+  TRY(build_gemms(m.get()));
+  *out = m.release();
+  return FADE_OK;
+}
+
+int fade_model_destroy(fade_model_t* m) {
+  if (!m) return FADE_OK;
+  cudaSetDevice(m->device);
+  cudaDeviceSynchronize();
+  cudaFree(m->mem);
+  for (auto& e : m->ev) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(m->ev_cum[i]);
+    cudaEventDestroy(m->ev_enc[i]);
+  }
+  cudaEventDestroy(m->ev_side_done);
+  cudaEventDestroy(m->ev_coder_join);
+  cudaStreamDestroy(m->s_main);
+  cudaStreamDestroy(m->s_side);
+  cudaStreamDestroy(m->s_coder);
+  delete m;
+  return FADE_OK;
+}
+
+static float* tensor_base(fade_model_t* m, int kind, int index) {
+  const Tensor4& t = m->M.w[index];
+  switch (kind) {
+    case 0: return t.p;
+    case 1: return t.m;
+    case 2: return t.v;
+    case 3: return t.g;
+  }
+  return nullptr;
+}
+
+// w_e1 / w_e2 live interleaved in W12 (model.cuh): 64-column blocks
+static int copy_w12(fade_model_t* m, float* dev, int which, float* host, bool to_dev) {
+  const Dims& d = m->d;
+  const size_t dpitch = sizeof(float) * 2 * d.Ep, spitch = sizeof(float) * d.E;
+  for (int j = 0; j * 64 < d.E; ++j) {
+    const int w = std::min(64, d.E - 64 * j);
+    float* dptr = dev + 128 * j + 64 * which;
+    float* hptr = host + 64 * j;
+    cudaError_t e = to_dev ? cudaMemcpy2D(dptr, dpitch, hptr, spitch, sizeof(float) * w, d.H,
+                                          cudaMemcpyHostToDevice)
+                           : cudaMemcpy2D(hptr, spitch, dptr, dpitch, sizeof(float) * w, d.H,
+                                          cudaMemcpyDeviceToHost);
+    CK(e);
+  }
+  return FADE_OK;
+}
+
+int fade_model_set_tensor(fade_model_t* m, int kind, int index, const float* host, int64_t n) {
+  if (index < 0 || index >= P_COUNT || kind < 0 || kind > 3 || n != ref_numel(m->d, index)) {
+    set_last_error("set_tensor: bad kind/index/size");
+    return FADE_ERR_USAGE;
+  }
+  CK(cudaSetDevice(m->device));
+  float* dev = tensor_base(m, kind, index);
+  if (index == P_W_E1 || index == P_W_E2)
+    return copy_w12(m, dev, index == P_W_E2, const_cast<float*>(host), true);
+  CK(cudaMemcpy(dev, host, sizeof(float) * n, cudaMemcpyHostToDevice));
+  return FADE_OK;
+}
+
+int fade_model_get_tensor(fade_model_t* m, int kind, int index, float* host, int64_t n) {
+  if (index < 0 || index >= P_COUNT || kind < 0 || kind > 3 || n != ref_numel(m->d, index)) {
+    set_last_error("get_tensor: bad kind/index/size");
+    return FADE_ERR_USAGE;
+  }
+  CK(cudaSetDevice(m->device));
+  CK(cudaDeviceSynchronize());
+  float* dev = tensor_base(m, kind, index);
+  if (index == P_W_E1 || index == P_W_E2) return copy_w12(m, dev, index == P_W_E2, host, false);
+  CK(cudaMemcpy(host, dev, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  return FADE_OK;
+}
+
+int fade_model_set_cache(fade_model_t* m, const float* host) {
+  CK(cudaSetDevice(m->device));
+  CK(cudaMemcpy(m->M.a.cache, host, sizeof(float) * m->d.B * m->d.C, cudaMemcpyHostToDevice));
+  return FADE_OK;
+}
+
+int fade_model_get_cache(fade_model_t* m, float* host) {
+  CK(cudaSetDevice(m->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(host, m->M.a.cache, sizeof(float) * m->d.B * m->d.C, cudaMemcpyDeviceToHost));
+  return FADE_OK;
+}
+
+int fade_model_set_counters(fade_model_t* m, int64_t adam_t, int64_t step_count) {
+  CK(cudaSetDevice(m->device));
+  long long v[2] = {adam_t, step_count};
+  CK(cudaMemcpy(&m->st->adam_t, &v[0], sizeof(long long), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(&m->st->step_count, &v[1], sizeof(long long), cudaMemcpyHostToDevice));
+  return FADE_OK;
+}
+
+int fade_model_get_counters(fade_model_t* m, int64_t* adam_t, int64_t* step_count) {
+  CK(cudaSetDevice(m->device));
+  CK(cudaDeviceSynchronize());
+  long long v[2];
+  CK(cudaMemcpy(&v[0], &m->st->adam_t, sizeof(long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&v[1], &m->st->step_count, sizeof(long long), cudaMemcpyDeviceToHost));
+  *adam_t = v[0];
+  *step_count = v[1];
+  return FADE_OK;
+}
+
+static StepIO api_io(fade_model_t* m) {
+  StepIO io{};
+  io.src = m->ctx_buf;
+  io.ld_src = m->d.T;
+  io.use_col = 0;
+  return io;
+}
+
+int fade_model_predict(fade_model_t* m, const uint8_t* ctx, double* probs, double* alpha,
+                       fade_error_t* err) {
+  CK(cudaSetDevice(m->device));
+  const Dims& d = m->d;
+  int64_t sc = 0, t = 0;
+  TRY(fade_model_get_counters(m, &t, &sc));
+  TRY(set_col(m, sc, sc));
+  CK(cudaMemcpyAsync(m->ctx_buf, ctx, (size_t)d.B * d.T, cudaMemcpyHostToDevice, m->s_main));
+  StepIO io = api_io(m);
+  io.head.want_probs = 1;
+  TRY(forward(m, io, true));
+  CK(cudaStreamSynchronize(m->s_main));
+  TRY(check_error(m, err));
+  if (probs)
+    CK(cudaMemcpy(probs, m->M.a.probs, sizeof(double) * d.B * 256, cudaMemcpyDeviceToHost));
+  if (alpha) {
+    std::vector<float> rows(3 * (size_t)d.B);
+    CK(cudaMemcpy(rows.data(), m->M.a.alpha_row, sizeof(float) * rows.size(), cudaMemcpyDeviceToHost));
+    double s = 0.0, mn = rows[1], mx = rows[2];
+    for (int b = 0; b < d.B; ++b) {
+      s += rows[3 * b];
+      mn = std::min(mn, (double)rows[3 * b + 1]);
+      mx = std::max(mx, (double)rows[3 * b + 2]);
+    }
+    alpha[0] = s / ((double)d.B * d.H);
+    alpha[1] = mn;
+    alpha[2] = mx;
+  }
+  m->live = true;
+  return FADE_OK;
+}
+
+int fade_model_train_step(fade_model_t* m, const uint8_t* targets, double* loss, fade_error_t* err) {
+  if (!m->live) {
+    set_last_error("train_step requires a preceding predict");
+    return FADE_ERR_STATE;
+  }
+  CK(cudaSetDevice(m->device));
+  const Dims& d = m->d;
+  CK(cudaMemcpyAsync(m->tgt_buf, targets, (size_t)d.B, cudaMemcpyHostToDevice, m->s_main));
+  StepIO io = api_io(m);
+  io.head.xent = 1;
+  io.head.tgt = m->tgt_buf;
+  io.head.ld_tgt = 1;
+  launch_head(m->M, io.head, m->s_main);     // dlogits + nll for these targets
+  TRY(backward(m, io, false, m->loss_buf));
+  launch_advance(m->M, 1, m->s_main);
+  CK(cudaStreamSynchronize(m->s_main));
+  TRY(check_error(m, err));
+  CK(cudaMemcpy(loss, m->loss_buf, sizeof(double), cudaMemcpyDeviceToHost));
+  m->live = false;
+  return FADE_OK;
+}
+
+static const float* part_ptr(fade_model_t* m, const char* part, int* width) {
+  const Acts& a = m->M.a;
+  *width = m->d.H;
+  std::string p(part);
+  if (p == "global") return a.h_g;
+  if (p == "local") return a.h_l;
+  if (p == "alpha") return a.alpha;
+  if (p == "mix") return a.h_mix;
+  if (p == "mixer_inner") return a.inner;
+  if (p == "coarse") return a.h_c;
+  if (p == "hidden") return a.h;
+  if (p == "logits") { *width = 256; return a.logits; }
+  return nullptr;
+}
+
+int fade_model_forward_debug(fade_model_t* m, const uint8_t* ctx, const char* part, float* out) {
+  CK(cudaSetDevice(m->device));
+  int width = 0;
+  const float* src = part_ptr(m, part, &width);
+  if (!src) {
+    set_last_error(std::string("unknown forward part ") + part);
+    return FADE_ERR_USAGE;
+  }
+  const Dims& d = m->d;
+  const size_t cbytes = sizeof(float) * d.B * d.C;
+  CK(cudaMemcpyAsync(m->cache_snap, m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  CK(cudaMemcpyAsync(m->ctx_buf, ctx, (size_t)d.B * d.T, cudaMemcpyHostToDevice, m->s_main));
+  StepIO io = api_io(m);
+  TRY(forward(m, io, false));
+  CK(cudaMemcpyAsync(out, src, sizeof(float) * d.B * width, cudaMemcpyDeviceToHost, m->s_main));
+  CK(cudaMemcpyAsync(m->M.a.cache, m->cache_snap, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  CK(cudaStreamSynchronize(m->s_main));
+  return FADE_OK;
+}
+
+int fade_model_loss_grads(fade_model_t* m, const uint8_t* ctx, const uint8_t* targets, double* loss) {
+  CK(cudaSetDevice(m->device));
+  const Dims& d = m->d;
+  const size_t cbytes = sizeof(float) * d.B * d.C;
+  CK(cudaMemcpyAsync(m->cache_snap, m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  CK(cudaMemcpyAsync(m->ctx_buf, ctx, (size_t)d.B * d.T, cudaMemcpyHostToDevice, m->s_main));
+  CK(cudaMemcpyAsync(m->tgt_buf, targets, (size_t)d.B, cudaMemcpyHostToDevice, m->s_main));
+  int64_t sc = 0, t = 0;
+  TRY(fade_model_get_counters(m, &t, &sc));
+  TRY(set_col(m, sc, sc));
+  StepIO io = api_io(m);
+  io.head.xent = 1;
+  io.head.tgt = m->tgt_buf;
+  io.head.ld_tgt = 1;
+  TRY(forward(m, io, true));
+  TRY(backward(m, io, true, m->loss_buf));
+  CK(cudaMemcpyAsync(m->M.a.cache, m->cache_snap, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  CK(cudaStreamSynchronize(m->s_main));
+  TRY(check_error(m, nullptr));
+  CK(cudaMemcpy(loss, m->loss_buf, sizeof(double), cudaMemcpyDeviceToHost));
+  return FADE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// executors
+
+static int coder_create(int B, long long L, cudaStream_t s, fade_coder_t** out) {
+  std::unique_ptr<fade_coder> c(new fade_coder());
+  c->B = B;
+  c->L = L;
+  c->cap = 2 * L + 16;       // <= 2 bytes per symbol + the 5-shift flush
+  c->s = s;
+  const size_t nB = (size_t)B;
+  size_t off[8], total = 0;
+  const size_t sizes[8] = {8 * nB, 8 * nB, 4 * nB, 8 * nB, 8 * nB, nB * (size_t)c->cap, 8, 4};
+  for (int i = 0; i < 8; ++i) {
+    total = align_up(total, 256);
+    off[i] = total;
+    total += sizes[i];
+  }
+  CK(cudaMalloc(&c->mem, total));
+  char* base = (char*)c->mem;
+  c->e.low = (unsigned long long*)(base + off[0]);
+  c->e.rng = (unsigned long long*)(base + off[1]);
+  c->e.cache = (int*)(base + off[2]);
+  c->e.ncache = (long long*)(base + off[3]);
+  c->e.blen = (long long*)(base + off[4]);
+  c->e.buf = (uint8_t*)(base + off[5]);
+  c->e.col = (long long*)(base + off[6]);
+  c->e.done_blocks = (unsigned*)(base + off[7]);
+  c->e.cap = c->cap;
+  launch_enc_init(c->e, B, s);
+  CK(cudaGetLastError());
+  *out = c.release();
+  return FADE_OK;
+}
+
+int fade_coder_destroy(fade_coder_t* c) {
+  if (!c) return FADE_OK;
+  cudaFree(c->mem);
+  delete c;
+  return FADE_OK;
+}
+
+int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes) {
+  long long total = 0;
+  std::vector<long long> off(c->B);
+  for (int b = 0; b < c->B; ++b) {
+    off[b] = total;
+    total += c->lengths[b];
+  }
+  if (nbytes != total) {
+    set_last_error("coder_fetch: payload size mismatch");
+    return FADE_ERR_USAGE;
+  }
+  if (total == 0) return FADE_OK;
+  long long* doff = nullptr;
+  uint8_t* dout = nullptr;
+  CK(cudaMalloc(&doff, sizeof(long long) * c->B));
+  CK(cudaMalloc(&dout, (size_t)total));
+  CK(cudaMemcpy(doff, off.data(), sizeof(long long) * c->B, cudaMemcpyHostToDevice));
+  launch_compact(c->e, c->B, doff, dout, c->s);
+  CK(cudaStreamSynchronize(c->s));
+  CK(cudaMemcpy(payload, dout, (size_t)total, cudaMemcpyDeviceToHost));
+  cudaFree(doff);
+  cudaFree(dout);
+  return FADE_OK;
+}
+
+// one compression timestep; captured once into a CUDA graph and replayed
+static int compress_step(fade_model_t* m, fade_coder_t* c, const uint8_t* data, long long L,
+                         int pipelined, double* losses) {
+  StepIO io{};
+  io.src = data;
+  io.ld_src = L;
+  io.use_col = 1;
+  io.head.xent = 1;
+  io.head.tgt = data;
+  io.head.ld_tgt = L;
+  io.head.tgt_use_col = 1;
+  TRY(forward(m, io, true));
+  if (pipelined) {
+    // CSPP: the coder stream drains this step's table while the model
+    // stream runs the backward (pipeline.py:251-287)
+    CK(cudaEventRecord(m->ev_cum[0], m->s_main));
+    CK(cudaStreamWaitEvent(m->s_coder, m->ev_cum[0], 0));
+    launch_encode_col(c->e, m->d.B, data, L, m->M.a.cum, m->s_coder);
+    CK(cudaEventRecord(m->ev_enc[0], m->s_coder));
+  } else {
+    launch_encode_col(c->e, m->d.B, data, L, m->M.a.cum, m->s_main);
+  }
+  TRY(backward(m, io, false, losses));
+  if (pipelined) CK(cudaStreamWaitEvent(m->s_main, m->ev_enc[0], 0));
+  launch_advance(m->M, 1, m->s_main);
+  CK(cudaGetLastError());
+  return FADE_OK;
+}
+
+int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, int64_t warm,
+                  int on_device, int pipelined, int64_t* lengths, double* losses, double* alpha,
+                  fade_coder_t** coder_out, fade_error_t* err) {
+  (void)alpha;
+  *coder_out = nullptr;
+  if (m && m->d.B != batch) {
+    set_last_error("compress: batch does not match the model");
+    return FADE_ERR_USAGE;
+  }
+  if (!m && L > warm) {
+    set_last_error("compress: a model is required when L > warm");
+    return FADE_ERR_USAGE;
+  }
+  cudaStream_t s = m ? m->s_main : nullptr;
+  if (m) CK(cudaSetDevice(m->device));
+  const size_t nbytes = (size_t)batch * (size_t)L;
+  uint8_t* dmat = nullptr;
+  const uint8_t* mat = data;
+  if (!on_device && nbytes) {
+    CK(cudaMalloc(&dmat, nbytes));
+    CK(cudaMemcpyAsync(dmat, data, nbytes, cudaMemcpyHostToDevice, s));
+    mat = dmat;
+  }
+  fade_coder_t* c = nullptr;
+  TRY(coder_create(batch, L, s, &c));
+  std::unique_ptr<fade_coder> guard(c);
+  launch_encode_warm(c->e, batch, mat, L, warm, s);
+  double* dloss = nullptr;
+  int status = FADE_OK;
+  if (m && L > warm) {
+    TRY(set_col(m, warm, warm));
+    CK(cudaMalloc(&dloss, sizeof(double) * (size_t)(L - warm)));
+    // capture one timestep into a graph, replay it L - warm times
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
+    status = compress_step(m, c, mat, L, pipelined, dloss);
+    cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
+    if (status != FADE_OK) return status;
+    CK(ce);
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    // the coder's column counter must start where the model does
+    for (long long i = warm; i < L; ++i) CK(cudaGraphLaunch(exec, m->s_main));
+    CK(cudaStreamSynchronize(m->s_main));
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    status = check_error(m, err);
+    if (status == FADE_OK && losses)
+      CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)(L - warm), cudaMemcpyDeviceToHost));
+    cudaFree(dloss);
+  }
+  launch_encode_flush(c->e, batch, s);
+  c->lengths.resize(batch);
+  CK(cudaMemcpyAsync(c->lengths.data(), c->e.blen, sizeof(long long) * batch,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (dmat) cudaFree(dmat);
+  if (status != FADE_OK) return status;
+  for (int b = 0; b < batch; ++b) lengths[b] = c->lengths[b];
+  *coder_out = guard.release();
+  return FADE_OK;
+}
+
+int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t nbytes,
+                    const int64_t* lengths, int64_t L, int64_t warm, uint8_t* out, double* losses,
+                    fade_error_t* err) {
+  if (m && m->d.B != batch) {
+    set_last_error("decompress: batch does not match the model");
+    return FADE_ERR_USAGE;
+  }
+  if (!m && L > warm) {
+    set_last_error("decompress: a model is required when L > warm");
+    return FADE_ERR_USAGE;
+  }
+  cudaStream_t s = m ? m->s_main : nullptr;
+  if (m) CK(cudaSetDevice(m->device));
+  // device copies: payload, offsets, lengths, decoder state, output matrix
+  std::vector<long long> off(batch);
+  long long tot = 0;
+  for (int b = 0; b < batch; ++b) {
+    off[b] = tot;
+    tot += lengths[b];
+  }
+  if (tot != nbytes) {
+    set_last_error("decompress: payload length does not match the stream table");
+    return FADE_ERR_USAGE;
+  }
+  const size_t nB = (size_t)batch;
+  const size_t sizes[8] = {(size_t)std::max<long long>(nbytes, 1), 8 * nB, 8 * nB, 8 * nB,
+                           8 * nB, 8 * nB, (size_t)batch * (size_t)L + 1, 8};
+  size_t offs[8], total = 0;
+  for (int i = 0; i < 8; ++i) {
+    total = align_up(total, 256);
+    offs[i] = total;
+    total += sizes[i];
+  }
+  void* mem = nullptr;
+  CK(cudaMalloc(&mem, total));
+  char* base = (char*)mem;
+  DecState ds;
+  ds.payload = (const uint8_t*)(base + offs[0]);
+  ds.off = (const long long*)(base + offs[1]);
+  ds.dlen = (const long long*)(base + offs[2]);
+  ds.pos = (long long*)(base + offs[3]);
+  ds.code = (unsigned long long*)(base + offs[4]);
+  ds.rng = (unsigned long long*)(base + offs[5]);
+  uint8_t* dmat = (uint8_t*)(base + offs[6]);
+  unsigned long long* err_key = m ? &m->st->err_key : (unsigned long long*)(base + offs[7]);
+  if (nbytes) CK(cudaMemcpyAsync((void*)ds.payload, payload, nbytes, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync((void*)ds.off, off.data(), 8 * nB, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync((void*)ds.dlen, lengths, 8 * nB, cudaMemcpyHostToDevice, s));
+  if (!m) {
+    unsigned long long none = ~0ull;
+    CK(cudaMemcpyAsync(err_key, &none, 8, cudaMemcpyHostToDevice, s));
+  }
+  launch_dec_prime(ds, batch, err_key, s);
+  launch_decode_warm(ds, batch, dmat, L, warm, err_key, s);
+  int status = FADE_OK;
+  double* dloss = nullptr;
+  if (m && L > warm) {
+    TRY(set_col(m, warm, warm));
+    CK(cudaMalloc(&dloss, sizeof(double) * (size_t)(L - warm)));
+    StepIO io{};
+    io.src = dmat;
+    io.ld_src = L;
+    io.use_col = 1;
+    io.head.xent = 1;
+    io.head.decode = 1;
+    io.head.out = dmat;
+    io.head.ld_out = L;
+    io.head.payload = ds.payload;
+    io.head.off = ds.off;
+    io.head.dlen = ds.dlen;
+    io.head.dpos = ds.pos;
+    io.head.dcode = ds.code;
+    io.head.drng = ds.rng;
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
+    // decode(i) -> train(i) -> predict(i+1) is strictly serial (pipeline.py:364-376)
+    status = forward(m, io, true);
+    if (status == FADE_OK) status = backward(m, io, false, dloss);
+    launch_advance(m->M, 1, m->s_main);
+    cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
+    if (status != FADE_OK) return status;
+    CK(ce);
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    for (long long i = warm; i < L; ++i) CK(cudaGraphLaunch(exec, m->s_main));
+    CK(cudaStreamSynchronize(m->s_main));
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+  }
+  CK(cudaStreamSynchronize(s));
+  if (m) {
+    status = check_error(m, err);
+  } else {
+    unsigned long long key = 0;
+    CK(cudaMemcpy(&key, err_key, 8, cudaMemcpyDeviceToHost));
+    if (key != ~0ull) {
+      const int code = (int)(key & 7);
+      err->kind = FADE_ERR_CORRUPT;
+      err->why = code == 1 ? 1 : 2;
+      err->stream = (long long)((key >> 3) & ((1ull << 21) - 1));
+      err->step = code == 6 ? -1 : (long long)(key >> 24);
+      set_last_error(code == 6 ? "stream shorter than coder tail"
+                               : (code == 1 ? "invalid code value" : "truncated stream"));
+      status = FADE_ERR_CORRUPT;
+    }
+  }
+  if (status == FADE_OK) {
+    CK(cudaMemcpy(out, dmat, (size_t)batch * (size_t)L, cudaMemcpyDeviceToHost));
+    if (losses && dloss)
+      CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)(L - warm), cudaMemcpyDeviceToHost));
+  }
+  if (dloss) cudaFree(dloss);
+  cudaFree(mem);
+  return status;
+}
+
+int fade_bench_compress_steps(fade_model_t* m, const uint8_t* data_dev, int64_t L, int64_t start,
+                              int64_t steps, fade_coder_t** coder, int* launches, void* stream) {
+  (void)stream;
+  CK(cudaSetDevice(m->device));
+  if (!*coder) {
+    TRY(coder_create(m->d.B, L, m->s_main, coder));
+    TRY(set_col(m, start, start));
+    long long v = start;
+    CK(cudaMemcpy((*coder)->e.col, &v, sizeof(v), cudaMemcpyHostToDevice));
+  }
+  static thread_local cudaGraphExec_t exec = nullptr;
+  static thread_local fade_model_t* exec_owner = nullptr;
+  if (exec_owner != m || !exec) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
+    int status = compress_step(m, *coder, data_dev, L, 1, nullptr);
+    cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
+    if (status != FADE_OK) return status;
+    CK(ce);
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    size_t n = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &n));
+    m->launches_per_step = (int)n;
+    cudaGraphDestroy(graph);
+    exec_owner = m;
+  }
+  for (long long i = 0; i < steps; ++i) CK(cudaGraphLaunch(exec, m->s_main));
+  if (launches) *launches = m->launches_per_step;
+  return FADE_OK;
+}
+
+}  // extern "C"

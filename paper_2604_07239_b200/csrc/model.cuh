@@ -1,0 +1,126 @@
+// Device-side model state and the fused row kernels of the FADE predictor.
+//
+// Data layout in HBM (fp32, row-major, one row per stream b):
+//   activations [B][ld] with ld = logical width (all widths are multiples of 4,
+//   ModelConfig.device_check), except the FNR expansion whose width E is padded
+//   to Ep = roundup(E, 64): the two expansion weights w_e1 / w_e2 are stored as
+//   ONE interleaved matrix W12[H][2*Ep] whose 128-column block j holds
+//   [w_e1[:, 64j:64j+64] | w_e2[:, 64j:64j+64]], so a 128-wide GEMM tile carries
+//   matching a1/a2 columns and the GeGLU runs in the GEMM epilogue.
+//   Padded columns are zero and stay zero (zero gradient => zero Adam step).
+#pragma once
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace fade {
+
+struct Dims {
+  int B, T, D, H, C, X, E, Ep, K;  // streams, ctx, embed, hidden, cache, mix, expand, padded, conv
+};
+
+// reference parameter order (model.py:76-105)
+enum ParamId {
+  P_EMB = 0, P_IN_LN_G, P_IN_LN_B, P_W_GATE, P_W_VAL, P_W_MEM, P_LAM_MEM, P_LOC_LN_G,
+  P_LOC_LN_B, P_CONV_K, P_CONV_B, P_W_ROUTE, P_MIX_LN_G, P_MIX_LN_B, P_W_DOWN, P_W_MIX,
+  P_W_UP, P_W_CGATE, P_LAM_MIX, P_REF_LN_G, P_REF_LN_B, P_W_E1, P_W_E2, P_W_F, P_OUT_LN_G,
+  P_OUT_LN_B, P_LAM_OUT, P_W_HEAD, P_B_HEAD, P_COUNT
+};
+
+// Small parameters live contiguously in one arena in the order of the per-row
+// reduction buffer ("rowred"), so one column-sum kernel produces their
+// gradients and applies Adam in place.  Offsets (in floats) into that arena:
+struct SmallLayout {
+  int out_g, out_b, ref_g, ref_b, mix_g, mix_b, in_g, in_b;  // H each
+  int loc_g, loc_b, conv_b;                                  // D each
+  int conv_k;                                                // K*D*D
+  int w_gate, w_val;                                         // D*D each
+  int lam_out, lam_mix, lam_mem;                             // 1 each
+  int rowred;                                                // width of the rowred buffer
+  int b_head;                                                // 256, reduced from dlogits
+  int total;
+};
+
+struct Tensor4 {     // parameter, Adam m, Adam v, gradient (test hook)
+  float *p, *m, *v, *g;
+};
+
+struct StepState {   // device-resident, so one captured graph replays every step
+  long long col;        // current column of the stream matrix (timestep)
+  long long adam_t;     // Adam step count (optim.py:21 self.t)
+  long long step_count; // Predictor.step_count
+  long long loss_base;  // column whose loss goes to losses[0]
+  AdamScalars adam;
+  unsigned long long err_key;   // min over (step << 24 | stream << 3 | code); ~0 = none
+  double alpha_sum, alpha_min, alpha_max;   // last predict's router stats
+};
+
+struct Acts {        // saved activations and gradient scratch, all [B][ld]
+  // forward
+  float *x, *x_hat, *x_inv, *gpre, *vpre, *loc, *loc_hat, *loc_inv, *conv_pre, *h_l;
+  float *cache;                 // [B][C] rolling cache (rolled in place each predict)
+  float *rpre, *ws_mem, *upre, *h_g, *alpha, *h_mix, *z_hat, *z_inv, *z;
+  float *zd, *u, *inner, *cpre, *gate, *h_c, *z2_hat, *z2_inv, *z2;
+  float *a12, *wide, *ws_f, *n_hat, *n_inv, *nrm, *h, *logits;
+  double *probs;                // [B][256] (predict API only)
+  unsigned *cum;                // [2][B][kCumLd] CSPP slots
+  double *nll;                  // [B]
+  float *alpha_row;             // [B][3] per-row router stats (sum, min, max)
+  // backward
+  float *dlogits, *dh, *dhc, *dnpre, *da12, *ws_dz2, *dinner, *dcpre, *du, *dhm_c;
+  float *dzd, *dz, *drpre, *dupre, *dh_l, *dx_part, *dx_r, *dblock, *demb;
+  float *rowred;                // [B][rowred]
+  float *emb_part;              // [chunks][256][D]
+};
+
+struct ModelPtrs {   // everything a row kernel may need, passed by value
+  Dims d;
+  SmallLayout sl;
+  Tensor4 w[P_COUNT];  // for small params these point into the small arena
+  float* small_p; float* small_m; float* small_v; float* small_g;
+  Acts a;
+  StepState* st;
+  int splits_mem, splits_f, splits_dz2;
+  int emb_chunk;       // streams per embedding-gradient partial
+};
+
+// row kernels (model_kernels.cu)
+void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                      cudaStream_t s);
+void launch_mix_fwd(const ModelPtrs& M, cudaStream_t s);
+void launch_bmm_fwd(const ModelPtrs& M, cudaStream_t s);
+void launch_coarse_fwd(const ModelPtrs& M, cudaStream_t s);
+void launch_out_fwd(const ModelPtrs& M, cudaStream_t s);
+// head: fp64 softmax -> quantiser -> cum slot; optional probs; optional
+// cross-entropy with targets read from tgt (+ col) or decoded in place.
+struct HeadArgs {
+  int want_probs;
+  int xent;                 // 1: emit dlogits + nll
+  const uint8_t* tgt;       // target bytes (row b at tgt + b*ld_tgt + col) or null
+  long long ld_tgt;
+  int tgt_use_col;
+  // decoder (decompression: decode the symbol of each stream from this table)
+  int decode;
+  uint8_t* out;             // decoded byte -> out[b*ld_out + col]
+  long long ld_out;
+  const uint8_t* payload;
+  const long long* off;
+  const long long* dlen;
+  long long* dpos;
+  unsigned long long* dcode;
+  unsigned long long* drng;
+};
+void launch_head(const ModelPtrs& M, const HeadArgs& h, cudaStream_t s);
+void launch_adam_prep(const ModelPtrs& M, double lr, double b1, double b2, double eps,
+                      cudaStream_t s);
+void launch_out_bwd(const ModelPtrs& M, cudaStream_t s);
+void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s);
+void launch_bmm_bwd(const ModelPtrs& M, int grad_only, cudaStream_t s);
+void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s);
+void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                      cudaStream_t s);
+void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, cudaStream_t s);
+void launch_emb_grad(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                     int grad_only, cudaStream_t s);
+void launch_advance(const ModelPtrs& M, int trained, cudaStream_t s);
+
+}  // namespace fade

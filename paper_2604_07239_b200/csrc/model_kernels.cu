@@ -1,0 +1,849 @@
+// Fused row kernels of the FADE predictor (one CTA per stream row).
+//
+// Forward follows pkg/src/dszip/model.py:109-179 and the op definitions of
+// pkg/src/dszip/nn/ops.py; backward restates the autograd closures of the same
+// ops.  Every reduction is a fixed-order tree (no atomics on values), so the
+// encoder and the decoder regenerate bit-identical probabilities.
+#include "coder.cuh"
+#include "model.cuh"
+
+namespace fade {
+
+constexpr int kRowThreads = 128;
+
+// LayerNorm statistics of a row held in shared memory (ops.py:94-101):
+// mu = mean(x); var = mean((x-mu)^2); inv = 1/sqrt(var + eps)
+__device__ __forceinline__ void ln_stats(const float* xs, int n, float* red, float* mu_out,
+                                         float* inv_out) {
+  float s = 0.f;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) s += xs[j];
+  const float mu = block_sum<kRowThreads / 32>(s, red) / (float)n;
+  float q = 0.f;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const float c = xs[j] - mu;
+    q += c * c;
+  }
+  const float var = block_sum<kRowThreads / 32>(q, red) / (float)n;
+  *mu_out = mu;
+  *inv_out = __fdiv_rn(1.0f, __fsqrt_rn(var + kLnEps));
+}
+
+// LayerNorm backward over one row (ops.py:103-113): returns dx into dxs (smem or
+// regs written by caller).  g = upstream grad (smem), xhat (global row), gain.
+__device__ __forceinline__ void ln_bwd_means(const float* gs, const float* xhat_row,
+                                             const float* gain, int n, float* red, float* m1,
+                                             float* m2) {
+  float s1 = 0.f, s2 = 0.f;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const float gg = gs[j] * gain[j];
+    s1 += gg;
+    s2 += gg * xhat_row[j];
+  }
+  *m1 = block_sum<kRowThreads / 32>(s1, red) / (float)n;
+  *m2 = block_sum<kRowThreads / 32>(s2, red) / (float)n;
+}
+
+// ---------------------------------------------------------------------------
+// trunk + local stream forward (model.py:118-137)
+__global__ void __launch_bounds__(kRowThreads) k_trunk_fwd(ModelPtrs M, const uint8_t* src,
+                                                           long long ld_src, int use_col) {
+  const Dims d = M.d;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* es = sm;                         // raw embedding row [H]
+  float* xs = es + d.H;                   // x row [H]
+  float* locs = xs + d.H;                 // LN_D(emb) row [H]
+  float* wg = locs + d.H;                 // [D*D]
+  float* wv = wg + d.D * d.D;             // [D*D]
+  float* ck = wv + d.D * d.D;             // [K*D*D]
+  float* blk = ck + d.K * d.D * d.D;      // [D]
+  float* tmu = blk + d.D;                 // [T]
+  float* tinv = tmu + d.T;                // [T]
+  float* red = tinv + d.T;                // [32]
+  int* ctx = (int*)(red + 32);            // [T]
+
+  const long long c0 = use_col ? M.st->col - d.T : 0;
+  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
+  for (int j = tid; j < d.D * d.D; j += blockDim.x) {
+    wg[j] = M.w[P_W_GATE].p[j];
+    wv[j] = M.w[P_W_VAL].p[j];
+  }
+  for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) ck[j] = M.w[P_CONV_K].p[j];
+  __syncthreads();
+
+  // embedding gather + input LayerNorm over the flattened window
+  const float* E = M.w[P_EMB].p;
+  for (int j = tid; j < d.H; j += blockDim.x) es[j] = E[ctx[j / d.D] * d.D + (j % d.D)];
+  __syncthreads();
+  float mu, inv;
+  ln_stats(es, d.H, red, &mu, &inv);
+  const float* g_in = M.w[P_IN_LN_G].p;
+  const float* b_in = M.w[P_IN_LN_B].p;
+  const long long rH = (long long)b * d.H;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float xh = (es[j] - mu) * inv;
+    const float xv = xh * g_in[j] + b_in[j];
+    xs[j] = xv;
+    M.a.x_hat[rH + j] = xh;
+    M.a.x[rH + j] = xv;
+  }
+  if (tid == 0) M.a.x_inv[b] = inv;
+  __syncthreads();
+
+  // GeGLU block of the newest symbol: gelu(x_t W_gate) * (x_t W_val)
+  const float* xt = xs + (d.H - d.D);
+  for (int o = tid; o < d.D; o += blockDim.x) {
+    float g = 0.f, v = 0.f;
+    for (int i = 0; i < d.D; ++i) {
+      g += xt[i] * wg[i * d.D + o];
+      v += xt[i] * wv[i * d.D + o];
+    }
+    M.a.gpre[(long long)b * d.D + o] = g;
+    M.a.vpre[(long long)b * d.D + o] = v;
+    blk[o] = gelu_f(g) * v;
+  }
+  // roll the cache in place: new[j] = old[j + D]; new[C-D+o] = block[o]
+  {
+    float* crow = M.a.cache + (long long)b * d.C;
+    const int n4 = (d.C - d.D) / 4;      // float4 count to move
+    constexpr int U = 4;
+    for (int base = 0; base < n4; base += U * kRowThreads) {
+      float4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = base + u * kRowThreads + tid;
+        if (q < n4) r[u] = *(const float4*)(crow + d.D + 4 * q);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = base + u * kRowThreads + tid;
+        if (q < n4) *(float4*)(crow + 4 * q) = r[u];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    for (int o = tid; o < d.D; o += blockDim.x) crow[d.C - d.D + o] = blk[o];
+  }
+
+  // local stream: per-symbol LayerNorm over D (ops.py:94-101 on (B,T,D))
+  for (int t = tid; t < d.T; t += blockDim.x) {
+    float s = 0.f;
+    for (int e = 0; e < d.D; ++e) s += es[t * d.D + e];
+    const float m = s / (float)d.D;
+    float q = 0.f;
+    for (int e = 0; e < d.D; ++e) {
+      const float c = es[t * d.D + e] - m;
+      q += c * c;
+    }
+    tmu[t] = m;
+    tinv[t] = __fdiv_rn(1.0f, __fsqrt_rn(q / (float)d.D + kLnEps));
+    M.a.loc_inv[(long long)b * d.T + t] = tinv[t];
+  }
+  __syncthreads();
+  const float* lg = M.w[P_LOC_LN_G].p;
+  const float* lb = M.w[P_LOC_LN_B].p;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const int t = j / d.D, e = j % d.D;
+    const float lh = (es[j] - tmu[t]) * tinv[t];
+    const float lv = lh * lg[e] + lb[e];
+    locs[j] = lv;
+    M.a.loc_hat[rH + j] = lh;
+    M.a.loc[rH + j] = lv;
+  }
+  __syncthreads();
+  // same-padded conv, taps in ascending order (ops.py:57-72), then gelu
+  const float* cb = M.w[P_CONV_B].p;
+  const int pad = d.K / 2;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const int t = j / d.D, co = j % d.D;
+    float acc = cb[co];
+    for (int tap = 0; tap < d.K; ++tap) {
+      const int s = t + tap - pad;
+      if (s < 0 || s >= d.T) continue;
+      float part = 0.f;
+      const float* lrow = locs + s * d.D;
+      const float* kc = ck + tap * d.D * d.D + co;
+      for (int ci = 0; ci < d.D; ++ci) part += lrow[ci] * kc[ci * d.D];
+      acc += part;
+    }
+    M.a.conv_pre[rH + j] = acc;
+    M.a.h_l[rH + j] = gelu_f(acc);
+  }
+}
+
+void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                      cudaStream_t s) {
+  const Dims& d = M.d;
+  const size_t smem = sizeof(float) * (3 * d.H + (2 + d.K) * d.D * d.D + d.D + 2 * d.T + 32) +
+                      sizeof(int) * d.T;
+  k_trunk_fwd<<<d.B, kRowThreads, smem, s>>>(M, src, ld_src, use_col);
+}
+
+// ---------------------------------------------------------------------------
+// global stream finish + router + mixer LayerNorm (model.py:128-153)
+__global__ void __launch_bounds__(kRowThreads) k_mix_fwd(ModelPtrs M) {
+  const Dims d = M.d;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* hm = sm;            // h_mix row
+  float* red = hm + d.H;
+  const long long rH = (long long)b * d.H;
+  const long long plane = (long long)d.B * d.H;
+  const float lam = M.w[P_LAM_MEM].p[0];
+  float asum = 0.f, amin = 3.4e38f, amax = -3.4e38f;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    float up = 0.f;
+    for (int s = 0; s < M.splits_mem; ++s) up += M.a.ws_mem[s * plane + rH + j];
+    const float hg = gelu_f(up) + M.a.x[rH + j] * lam;
+    const float al = sigmoid_f(M.a.rpre[rH + j]);
+    const float hmx = al * hg + (1.0f - al) * M.a.h_l[rH + j];
+    M.a.upre[rH + j] = up;
+    M.a.h_g[rH + j] = hg;
+    M.a.alpha[rH + j] = al;
+    M.a.h_mix[rH + j] = hmx;
+    hm[j] = hmx;
+    asum += al;
+    amin = fminf(amin, al);
+    amax = fmaxf(amax, al);
+  }
+  __syncthreads();
+  // router statistics for the metrics tape (model.py:197-199)
+  {
+    const float s = block_sum<kRowThreads / 32>(asum, red);
+    float mn = warp_max(-amin), mx = warp_max(amax);
+    __shared__ float rmn[4], rmx[4];
+    if ((tid & 31) == 0) { rmn[tid >> 5] = mn; rmx[tid >> 5] = mx; }
+    __syncthreads();
+    if (tid == 0) {
+      float a = rmn[0], c = rmx[0];
+      for (int w = 1; w < kRowThreads / 32; ++w) { a = fmaxf(a, rmn[w]); c = fmaxf(c, rmx[w]); }
+      M.a.alpha_row[3 * b + 0] = s;
+      M.a.alpha_row[3 * b + 1] = -a;
+      M.a.alpha_row[3 * b + 2] = c;
+    }
+  }
+  float mu, inv;
+  ln_stats(hm, d.H, red, &mu, &inv);
+  const float* g = M.w[P_MIX_LN_G].p;
+  const float* bb = M.w[P_MIX_LN_B].p;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float zh = (hm[j] - mu) * inv;
+    M.a.z_hat[rH + j] = zh;
+    M.a.z[rH + j] = zh * g[j] + bb[j];
+  }
+  if (tid == 0) M.a.z_inv[b] = inv;
+}
+
+void launch_mix_fwd(const ModelPtrs& M, cudaStream_t s) {
+  k_mix_fwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+}
+
+// per-stream persistent memory: u[b] = zd[b] @ W_U[b]  (ops.py:44-54)
+__global__ void __launch_bounds__(kRowThreads) k_bmm_fwd(ModelPtrs M) {
+  const int X = M.d.X, b = blockIdx.x;
+  extern __shared__ float zs[];
+  for (int i = threadIdx.x; i < X; i += blockDim.x) zs[i] = M.a.zd[(long long)b * X + i];
+  __syncthreads();
+  const float* W = M.w[P_W_MIX].p + (long long)b * X * X;
+  for (int o = threadIdx.x; o < X; o += blockDim.x) {
+    float acc = 0.f;
+    for (int i = 0; i < X; ++i) acc += zs[i] * W[(long long)i * X + o];
+    M.a.u[(long long)b * X + o] = acc;
+  }
+}
+
+void launch_bmm_fwd(const ModelPtrs& M, cudaStream_t s) {
+  k_bmm_fwd<<<M.d.B, kRowThreads, sizeof(float) * M.d.X, s>>>(M);
+}
+
+// self-gated coarse refiner + FNR LayerNorm (model.py:156-167)
+__global__ void __launch_bounds__(kRowThreads) k_coarse_fwd(ModelPtrs M) {
+  const Dims d = M.d;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* hc = sm;
+  float* red = hc + d.H;
+  const long long rH = (long long)b * d.H;
+  const float lam = M.w[P_LAM_MIX].p[0];
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float gt = sigmoid_f(M.a.cpre[rH + j]);
+    const float v = M.a.inner[rH + j] * gt + M.a.h_mix[rH + j] * lam;
+    M.a.gate[rH + j] = gt;
+    M.a.h_c[rH + j] = v;
+    hc[j] = v;
+  }
+  __syncthreads();
+  float mu, inv;
+  ln_stats(hc, d.H, red, &mu, &inv);
+  const float* g = M.w[P_REF_LN_G].p;
+  const float* bb = M.w[P_REF_LN_B].p;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float zh = (hc[j] - mu) * inv;
+    M.a.z2_hat[rH + j] = zh;
+    M.a.z2[rH + j] = zh * g[j] + bb[j];
+  }
+  if (tid == 0) M.a.z2_inv[b] = inv;
+}
+
+void launch_coarse_fwd(const ModelPtrs& M, cudaStream_t s) {
+  k_coarse_fwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+}
+
+// FNR output: split-K reduce, LayerNorm, gelu, residual (model.py:170-172)
+__global__ void __launch_bounds__(kRowThreads) k_out_fwd(ModelPtrs M) {
+  const Dims d = M.d;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* np_ = sm;
+  float* red = np_ + d.H;
+  const long long rH = (long long)b * d.H;
+  const long long plane = (long long)d.B * d.H;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < M.splits_f; ++s) acc += M.a.ws_f[s * plane + rH + j];
+    np_[j] = acc;
+  }
+  __syncthreads();
+  float mu, inv;
+  ln_stats(np_, d.H, red, &mu, &inv);
+  const float* g = M.w[P_OUT_LN_G].p;
+  const float* bb = M.w[P_OUT_LN_B].p;
+  const float lam = M.w[P_LAM_OUT].p[0];
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float nh = (np_[j] - mu) * inv;
+    const float nv = nh * g[j] + bb[j];
+    M.a.n_hat[rH + j] = nh;
+    M.a.nrm[rH + j] = nv;
+    M.a.h[rH + j] = gelu_f(nv) + M.a.h_c[rH + j] * lam;
+  }
+  if (tid == 0) M.a.n_inv[b] = inv;
+}
+
+void launch_out_fwd(const ModelPtrs& M, cudaStream_t s) {
+  k_out_fwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+}
+
+// ---------------------------------------------------------------------------
+// head: fp64 softmax (ops.py:246-255) -> quantiser (kernels.py:48-85) ->
+// cumulative table (coder.py:37-43) -> [decode] -> softmax-xent (ops.py:258-279)
+__device__ __forceinline__ void record_error(StepState* st, long long step, long long stream,
+                                             int code) {
+  // lowest step first, then lowest stream; code 1/2 corrupt(why), 3 diverged,
+  // 4 quantiser, 5 non-finite loss
+  const unsigned long long key = ((unsigned long long)step << 24) |
+                                 ((unsigned long long)stream << 3) | (unsigned long long)code;
+  atomicMin((unsigned long long*)&st->err_key, key);
+}
+
+__device__ __forceinline__ double block_sum_d256(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum_d(v);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double t = lane < 8 ? red[lane] : 0.0;
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
+  __shared__ QuantSmem qs;
+  __shared__ double dred[8];
+  __shared__ unsigned cum_s[kAlphabet + 1];
+  __shared__ int wsum[8];
+  __shared__ int sym_s;
+  __shared__ int bad_s;
+  const int b = blockIdx.x, i = threadIdx.x;
+  StepState* st = M.st;
+  const long long col = st->col;
+  if (i == 0) bad_s = 0;
+  const float lg = M.a.logits[(long long)b * kAlphabet + i];
+  __syncthreads();
+  if (!isfinite(lg)) atomicOr(&bad_s, 1);
+  __syncthreads();
+  if (bad_s) {
+    if (i == 0) record_error(st, col, b, 3);
+    return;
+  }
+  // row max in float (exact), then z = logit - max in f64
+  const int lane = i & 31, w = i >> 5;
+  float mx = warp_max(lg);
+  __shared__ float fred[8];
+  if (lane == 0) fred[w] = mx;
+  __syncthreads();
+  mx = fred[0];
+  for (int k = 1; k < 8; ++k) mx = fmaxf(mx, fred[k]);
+  const double z = (double)lg - (double)mx;
+  const double e = exp(z);
+  const double s = block_sum_d256(e, dred);
+  const double p = e / s;
+  if (H.want_probs) M.a.probs[(long long)b * kAlphabet + i] = p;
+  bool qbad;
+  const int f = quantize_sym(p, qs, &qbad);
+  if (qbad) {
+    if (i == 0) record_error(st, col, b, 4);
+    return;
+  }
+  const int c = block_excl_scan256(f, wsum);
+  unsigned* cum = M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd;
+  cum[i] = (unsigned)c;
+  cum_s[i] = (unsigned)c;
+  if (i == kAlphabet - 1) {
+    cum[kAlphabet] = kTotal;
+    cum_s[kAlphabet] = kTotal;
+  }
+  __syncthreads();
+  if (!H.xent) return;
+  int tgt;
+  if (H.decode) {
+    if (i == 0) {
+      DecLane ln{H.dcode[b], H.drng[b], H.dpos[b]};
+      int sy = 0;
+      const int why = dec_symbol(ln, cum_s, H.payload + H.off[b], H.dlen[b], &sy);
+      if (why) {
+        record_error(st, col, b, why);
+        sy = 0;
+      } else {
+        H.dcode[b] = ln.code;
+        H.drng[b] = ln.rng;
+        H.dpos[b] = ln.pos;
+      }
+      H.out[(long long)b * H.ld_out + col] = (uint8_t)sy;
+      sym_s = sy;
+    }
+    __syncthreads();
+    tgt = sym_s;
+  } else {
+    tgt = H.tgt[(long long)b * H.ld_tgt + (H.tgt_use_col ? col : 0)];
+  }
+  // softmax_xent in f64: logp = z - log(sum exp z); grad = (p - onehot) / B
+  const double lse = log(s);
+  const double logp = z - lse;
+  double dgrad = exp(logp);
+  if (i == tgt) {
+    M.a.nll[b] = -logp;
+    dgrad -= 1.0;
+  }
+  dgrad *= 1.0 / (double)M.d.B;
+  M.a.dlogits[(long long)b * kAlphabet + i] = (float)dgrad;
+}
+
+void launch_head(const ModelPtrs& M, const HeadArgs& h, cudaStream_t s) {
+  k_head<<<M.d.B, 256, 0, s>>>(M, h);
+}
+
+// Adam bias-correction scalars from the device step counter (optim.py:26-30)
+__global__ void k_adam_prep(StepState* st, double lr, double b1, double b2, double eps) {
+  const long long t = ++st->adam_t;
+  const double c1 = 1.0 - pow(b1, (double)t);
+  const double c2 = 1.0 - pow(b2, (double)t);
+  AdamScalars a;
+  a.beta1 = (float)b1;
+  a.beta2 = (float)b2;
+  a.one_m_b1 = (float)(1.0 - b1);
+  a.one_m_b2 = (float)(1.0 - b2);
+  a.eps = (float)eps;
+  a.step_size = (float)(lr / c1);
+  a.inv_sqrt_c2 = 1.0 / sqrt(c2);
+  st->adam = a;
+}
+
+void launch_adam_prep(const ModelPtrs& M, double lr, double b1, double b2, double eps,
+                      cudaStream_t s) {
+  k_adam_prep<<<1, 1, 0, s>>>(M.st, lr, b1, b2, eps);
+}
+
+__device__ __forceinline__ void adam_update(const AdamScalars& a, float g, float* p, float* m,
+                                            float* v) {
+  const float m1 = __fadd_rn(__fmul_rn(*m, a.beta1), __fmul_rn(a.one_m_b1, g));
+  const float v1 = __fadd_rn(__fmul_rn(*v, a.beta2), __fmul_rn(a.one_m_b2, __fmul_rn(g, g)));
+  float sc = (float)__dmul_rn((double)__fsqrt_rn(v1), a.inv_sqrt_c2);
+  sc = __fadd_rn(sc, a.eps);
+  sc = __fmul_rn(__fdiv_rn(m1, sc), a.step_size);
+  *m = m1;
+  *v = v1;
+  *p = __fsub_rn(*p, sc);
+}
+
+// ---------------------------------------------------------------------------
+// backward row kernels
+
+// h = gelu(LN(npre)) + lam_out * h_c   (model.py:170-172 backward)
+__global__ void __launch_bounds__(kRowThreads) k_out_bwd(ModelPtrs M) {
+  const Dims d = M.d;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* dn = sm;
+  float* red = dn + d.H;
+  const long long rH = (long long)b * d.H;
+  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  const float lam = M.w[P_LAM_OUT].p[0];
+  float lsum = 0.f;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float dh = M.a.dh[rH + j];
+    const float v = dh * gelu_grad_f(M.a.nrm[rH + j]);
+    dn[j] = v;
+    rr[M.sl.out_g + j] = v * M.a.n_hat[rH + j];
+    rr[M.sl.out_b + j] = v;
+    lsum += dh * M.a.h_c[rH + j];
+    M.a.dhc[rH + j] = dh * lam;
+  }
+  __syncthreads();
+  const float ls = block_sum<kRowThreads / 32>(lsum, red);
+  if (tid == 0) rr[M.sl.lam_out] = ls;
+  float m1, m2;
+  const float* g = M.w[P_OUT_LN_G].p;
+  ln_bwd_means(dn, M.a.n_hat + rH, g, d.H, red, &m1, &m2);
+  const float inv = M.a.n_inv[b];
+  for (int j = tid; j < d.H; j += blockDim.x)
+    M.a.dnpre[rH + j] = (dn[j] * g[j] - m1 - M.a.n_hat[rH + j] * m2) * inv;
+}
+
+void launch_out_bwd(const ModelPtrs& M, cudaStream_t s) {
+  k_out_bwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+}
+
+// z2 = LN(h_c); h_c = inner * sigmoid(cpre) + lam_mix * h_mix   (backward)
+__global__ void __launch_bounds__(kRowThreads) k_coarse_bwd(ModelPtrs M) {
+  const Dims d = M.d;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* dz = sm;
+  float* red = dz + d.H;
+  const long long rH = (long long)b * d.H;
+  const long long plane = (long long)d.B * d.H;
+  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < M.splits_dz2; ++s) acc += M.a.ws_dz2[s * plane + rH + j];
+    dz[j] = acc;
+    rr[M.sl.ref_g + j] = acc * M.a.z2_hat[rH + j];
+    rr[M.sl.ref_b + j] = acc;
+  }
+  __syncthreads();
+  float m1, m2;
+  const float* g = M.w[P_REF_LN_G].p;
+  ln_bwd_means(dz, M.a.z2_hat + rH, g, d.H, red, &m1, &m2);
+  const float inv = M.a.z2_inv[b];
+  float lsum = 0.f;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float dhc = M.a.dhc[rH + j] + (dz[j] * g[j] - m1 - M.a.z2_hat[rH + j] * m2) * inv;
+    const float gt = M.a.gate[rH + j];
+    M.a.dhc[rH + j] = dhc;
+    M.a.dinner[rH + j] = dhc * gt;
+    M.a.dcpre[rH + j] = dhc * M.a.inner[rH + j] * gt * (1.0f - gt);
+    lsum += dhc * M.a.h_mix[rH + j];
+  }
+  const float ls = block_sum<kRowThreads / 32>(lsum, red);
+  if (tid == 0) rr[M.sl.lam_mix] = ls;
+}
+
+void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s) {
+  k_coarse_bwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+}
+
+// per-stream memory backward + its Adam step in one streaming pass
+// (ops.py:48-52 for the gradients, optim.py:25-44 for the update)
+__global__ void __launch_bounds__(kRowThreads) k_bmm_bwd(ModelPtrs M, int grad_only) {
+  const int X = M.d.X, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  extern __shared__ float sm[];
+  float* dus = sm;          // [X]
+  float* zds = sm + X;      // [X]
+  for (int i = threadIdx.x; i < X; i += blockDim.x) {
+    dus[i] = M.a.du[(long long)b * X + i];
+    zds[i] = M.a.zd[(long long)b * X + i];
+  }
+  __syncthreads();
+  const long long base = (long long)b * X * X;
+  float* Wp = M.w[P_W_MIX].p + base;
+  float* Wm = M.w[P_W_MIX].m + base;
+  float* Wv = M.w[P_W_MIX].v + base;
+  float* Wg = M.w[P_W_MIX].g + base;
+  const AdamScalars a = M.st->adam;
+  for (int i = w; i < X; i += kRowThreads / 32) {
+    float acc = 0.f;
+    for (int j = lane; j < X; j += 32) {
+      const long long q = (long long)i * X + j;
+      const float wv = Wp[q];
+      acc += dus[j] * wv;
+      const float g = zds[i] * dus[j];
+      if (grad_only) Wg[q] = g;
+      else adam_update(a, g, Wp + q, Wm + q, Wv + q);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) M.a.dzd[(long long)b * X + i] = acc;
+  }
+}
+
+void launch_bmm_bwd(const ModelPtrs& M, int grad_only, cudaStream_t s) {
+  k_bmm_bwd<<<M.d.B, kRowThreads, sizeof(float) * 2 * M.d.X, s>>>(M, grad_only);
+}
+
+// mixer LayerNorm + router mix + global-stream gelu (model.py:128-153 backward)
+__global__ void __launch_bounds__(kRowThreads) k_mix_bwd(ModelPtrs M) {
+  const Dims d = M.d;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* dz = sm;
+  float* red = dz + d.H;
+  const long long rH = (long long)b * d.H;
+  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float v = M.a.dz[rH + j];
+    dz[j] = v;
+    rr[M.sl.mix_g + j] = v * M.a.z_hat[rH + j];
+    rr[M.sl.mix_b + j] = v;
+  }
+  __syncthreads();
+  float m1, m2;
+  const float* g = M.w[P_MIX_LN_G].p;
+  ln_bwd_means(dz, M.a.z_hat + rH, g, d.H, red, &m1, &m2);
+  const float inv = M.a.z_inv[b];
+  const float lam_mix = M.w[P_LAM_MIX].p[0];
+  const float lam_mem = M.w[P_LAM_MEM].p[0];
+  float lsum = 0.f;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const float dhm = M.a.dhc[rH + j] * lam_mix + M.a.dhm_c[rH + j] +
+                      (dz[j] * g[j] - m1 - M.a.z_hat[rH + j] * m2) * inv;
+    const float al = M.a.alpha[rH + j];
+    const float dal = dhm * (M.a.h_g[rH + j] - M.a.h_l[rH + j]);
+    const float dhg = dhm * al;
+    M.a.dh_l[rH + j] = dhm * (1.0f - al);
+    M.a.drpre[rH + j] = dal * al * (1.0f - al);
+    M.a.dupre[rH + j] = dhg * gelu_grad_f(M.a.upre[rH + j]);
+    M.a.dx_part[rH + j] = dhg * lam_mem;
+    lsum += dhg * M.a.x[rH + j];
+  }
+  const float ls = block_sum<kRowThreads / 32>(lsum, red);
+  if (tid == 0) rr[M.sl.lam_mem] = ls;
+}
+
+void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s) {
+  k_mix_bwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+}
+
+// trunk + local stream backward (model.py:118-137 backward)
+__global__ void __launch_bounds__(kRowThreads) k_trunk_bwd(ModelPtrs M, const uint8_t* src,
+                                                           long long ld_src, int use_col) {
+  const Dims d = M.d;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  extern __shared__ float sm[];
+  float* dxs = sm;                        // [H] dx, later dxf
+  float* dcv = dxs + d.H;                 // [H] dconv
+  float* locs = dcv + d.H;                // [H] LN_D(emb) (conv input)
+  float* dls = locs + d.H;                // [H] dloc
+  float* ck = dls + d.H;                  // [K*D*D]
+  float* dg = ck + d.K * d.D * d.D;       // [D] dgpre
+  float* dv = dg + d.D;                   // [D] dvpre
+  float* xt = dv + d.D;                   // [D]
+  float* red = xt + d.D;                  // [32]
+  const long long rH = (long long)b * d.H;
+  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  const float* Wg = M.w[P_W_GATE].p;
+  const float* Wv = M.w[P_W_VAL].p;
+  for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) ck[j] = M.w[P_CONV_K].p[j];
+  for (int o = tid; o < d.D; o += blockDim.x) {
+    const float gp = M.a.gpre[(long long)b * d.D + o];
+    const float vp = M.a.vpre[(long long)b * d.D + o];
+    const float db = M.a.dblock[(long long)b * d.D + o];
+    dg[o] = db * vp * gelu_grad_f(gp);
+    dv[o] = db * gelu_f(gp);
+    xt[o] = M.a.x[rH + d.H - d.D + o];
+  }
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    dxs[j] = M.a.dx_r[rH + j] + M.a.dx_part[rH + j];
+    dcv[j] = M.a.dh_l[rH + j] * gelu_grad_f(M.a.conv_pre[rH + j]);
+    locs[j] = M.a.loc[rH + j];
+  }
+  __syncthreads();
+  // W_gate / W_val gradients (outer products) and dx_t
+  for (int q = tid; q < d.D * d.D; q += blockDim.x) {
+    const int i = q / d.D, o = q % d.D;
+    rr[M.sl.w_gate + q] = xt[i] * dg[o];
+    rr[M.sl.w_val + q] = xt[i] * dv[o];
+  }
+  for (int i = tid; i < d.D; i += blockDim.x) {
+    float a1 = 0.f, a2 = 0.f;
+    for (int o = 0; o < d.D; ++o) {
+      a1 += dg[o] * Wg[i * d.D + o];
+      a2 += dv[o] * Wv[i * d.D + o];
+    }
+    dxs[d.H - d.D + i] += a1 + a2;
+  }
+  __syncthreads();
+  // input LayerNorm backward
+  const float* gin = M.w[P_IN_LN_G].p;
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    rr[M.sl.in_g + j] = dxs[j] * M.a.x_hat[rH + j];
+    rr[M.sl.in_b + j] = dxs[j];
+  }
+  float m1, m2;
+  ln_bwd_means(dxs, M.a.x_hat + rH, gin, d.H, red, &m1, &m2);
+  const float xinv = M.a.x_inv[b];
+  for (int j = tid; j < d.H; j += blockDim.x)
+    dxs[j] = (dxs[j] * gin[j] - m1 - M.a.x_hat[rH + j] * m2) * xinv;   // dxf
+  // conv gradients: bias, taps, input (ops.py:74-88)
+  const int pad = d.K / 2;
+  for (int co = tid; co < d.D; co += blockDim.x) {
+    float s = 0.f;
+    for (int t = 0; t < d.T; ++t) s += dcv[t * d.D + co];
+    rr[M.sl.conv_b + co] = s;
+  }
+  for (int q = tid; q < d.K * d.D * d.D; q += blockDim.x) {
+    const int tap = q / (d.D * d.D), ci = (q / d.D) % d.D, co = q % d.D;
+    float s = 0.f;
+    for (int t = 0; t < d.T; ++t) {
+      const int sidx = t + tap - pad;
+      if (sidx >= 0 && sidx < d.T) s += locs[sidx * d.D + ci] * dcv[t * d.D + co];
+    }
+    rr[M.sl.conv_k + q] = s;
+  }
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const int sidx = j / d.D, ci = j % d.D;
+    float acc = 0.f;
+    for (int tap = 0; tap < d.K; ++tap) {
+      const int t = sidx - tap + pad;
+      if (t < 0 || t >= d.T) continue;
+      float part = 0.f;
+      for (int co = 0; co < d.D; ++co) part += dcv[t * d.D + co] * ck[(tap * d.D + ci) * d.D + co];
+      acc += part;
+    }
+    dls[j] = acc;
+  }
+  __syncthreads();
+  // per-symbol LayerNorm backward over D
+  const float* lg = M.w[P_LOC_LN_G].p;
+  for (int e = tid; e < d.D; e += blockDim.x) {
+    float s1 = 0.f, s2 = 0.f;
+    for (int t = 0; t < d.T; ++t) {
+      s1 += dls[t * d.D + e] * M.a.loc_hat[rH + t * d.D + e];
+      s2 += dls[t * d.D + e];
+    }
+    rr[M.sl.loc_g + e] = s1;
+    rr[M.sl.loc_b + e] = s2;
+  }
+  for (int t = tid; t < d.T; t += blockDim.x) {
+    float s1 = 0.f, s2 = 0.f;
+    for (int e = 0; e < d.D; ++e) {
+      const float gg = dls[t * d.D + e] * lg[e];
+      s1 += gg;
+      s2 += gg * M.a.loc_hat[rH + t * d.D + e];
+    }
+    // stash per-t means in the tail of locs (no longer needed after dloc)
+    locs[2 * t] = s1 / (float)d.D;
+    locs[2 * t + 1] = s2 / (float)d.D;
+  }
+  __syncthreads();
+  for (int j = tid; j < d.H; j += blockDim.x) {
+    const int t = j / d.D, e = j % d.D;
+    const float lh = M.a.loc_hat[rH + j];
+    const float de = (dls[j] * lg[e] - locs[2 * t] - lh * locs[2 * t + 1]) *
+                     M.a.loc_inv[(long long)b * d.T + t];
+    M.a.demb[rH + j] = de + dxs[j];
+  }
+}
+
+void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                      cudaStream_t s) {
+  const Dims& d = M.d;
+  const size_t smem = sizeof(float) * (4 * d.H + d.K * d.D * d.D + 3 * d.D + 32);
+  k_trunk_bwd<<<d.B, kRowThreads, smem, s>>>(M, src, ld_src, use_col);
+}
+
+// Column sums of the per-row reduction buffer + dlogits (b_head), in a fixed
+// order, then Adam on the small-parameter arena.  Also the step loss.
+constexpr int kColWarps = 32;
+__global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int grad_only,
+                                                               double* losses) {
+  __shared__ float part[kColWarps][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  const int R = M.sl.rowred;
+  const int total = R + kAlphabet;
+  float s = 0.f;
+  if (c < total) {
+    for (int b = w; b < M.d.B; b += kColWarps)
+      s += (c < R) ? M.a.rowred[(long long)b * R + c] : M.a.dlogits[(long long)b * kAlphabet + (c - R)];
+  }
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < total) {
+    float g = 0.f;
+    for (int k = 0; k < kColWarps; ++k) g += part[k][lane];
+    if (grad_only) M.small_g[c] = g;
+    else adam_update(M.st->adam, g, M.small_p + c, M.small_m + c, M.small_v + c);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 32) {
+    double l = 0.0;
+    for (int b = 0; b < M.d.B; ++b) l += M.a.nll[b];
+    l /= (double)M.d.B;
+    StepState* st = M.st;
+    if (!isfinite(l)) record_error(st, st->col, 0, 5);
+    if (losses) losses[st->col - st->loss_base] = l;
+  }
+}
+
+void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, cudaStream_t s) {
+  const int total = M.sl.rowred + kAlphabet;
+  k_small_adam<<<cdiv(total, 32), 32 * kColWarps, 0, s>>>(M, grad_only, losses);
+}
+
+// embedding gradient: deterministic two-level scatter-add (ops.py:234-243)
+__global__ void __launch_bounds__(256) k_emb_part(ModelPtrs M, const uint8_t* src,
+                                                  long long ld_src, int use_col) {
+  const Dims d = M.d;
+  extern __shared__ float acc[];          // [256][D]
+  const int chunk = blockIdx.x;
+  for (int q = threadIdx.x; q < kAlphabet * d.D; q += blockDim.x) acc[q] = 0.f;
+  __syncthreads();
+  const int groups = blockDim.x / d.D;
+  const int g = threadIdx.x / d.D, e = threadIdx.x % d.D;
+  const long long c0 = use_col ? M.st->col - d.T : 0;
+  const int b0 = chunk * M.emb_chunk, b1 = min(d.B, b0 + M.emb_chunk);
+  if (g < groups) {
+    for (int b = b0; b < b1; ++b) {
+      const uint8_t* row = src + (long long)b * ld_src + c0;
+      for (int t = 0; t < d.T; ++t) {
+        const int sym = row[t];
+        if (sym % groups != g) continue;
+        acc[sym * d.D + e] += M.a.demb[(long long)b * d.H + t * d.D + e];
+      }
+    }
+  }
+  __syncthreads();
+  float* out = M.a.emb_part + (long long)chunk * kAlphabet * d.D;
+  for (int q = threadIdx.x; q < kAlphabet * d.D; q += blockDim.x) out[q] = acc[q];
+}
+
+__global__ void k_emb_adam(ModelPtrs M, int nchunks, int grad_only) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = kAlphabet * M.d.D;
+  if (q >= n) return;
+  float g = 0.f;
+  for (int c = 0; c < nchunks; ++c) g += M.a.emb_part[(long long)c * n + q];
+  Tensor4 t = M.w[P_EMB];
+  if (grad_only) t.g[q] = g;
+  else adam_update(M.st->adam, g, t.p + q, t.m + q, t.v + q);
+}
+
+void launch_emb_grad(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                     int grad_only, cudaStream_t s) {
+  const int nchunks = cdiv(M.d.B, M.emb_chunk);
+  k_emb_part<<<nchunks, 256, sizeof(float) * kAlphabet * M.d.D, s>>>(M, src, ld_src, use_col);
+  k_emb_adam<<<cdiv(kAlphabet * M.d.D, 256), 256, 0, s>>>(M, nchunks, grad_only);
+}
+
+__global__ void k_advance(StepState* st, int trained) {
+  st->col += 1;
+  st->step_count += trained;
+}
+
+void launch_advance(const ModelPtrs& M, int trained, cudaStream_t s) {
+  k_advance<<<1, 1, 0, s>>>(M.st, trained);
+}
+
+}  // namespace fade

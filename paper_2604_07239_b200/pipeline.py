@@ -1,0 +1,316 @@
+"""Executors: stream partitioning, serial / pipelined compression and
+decompression, all running the whole timestep loop on the B200.
+
+Keeps the reference executor API (``pkg/src/dszip/pipeline.py:35-411``).  The
+difference is where the loop lives: the reference runs predict -> quantise ->
+encode -> train as Python calls on two host threads (model / coder) around a
+two-slot ping-pong buffer; here one ``fade_compress`` / ``fade_decompress`` call
+replays a captured CUDA graph per timestep.  The pipelined executor puts the
+encoder on its own CUDA stream, draining the step's cumulative-table slot while
+the model stream runs the backward pass -- the same two-slot protocol
+(empty -> filling -> full -> draining -> empty) enforced by CUDA events instead
+of a ``threading.Condition``.  Serial and pipelined produce identical bytes
+because the table for step i is always built before the step-i update.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .config import ModelConfig
+from .errors import CorruptionError, ModelDivergenceError
+from .model import LN2, Predictor
+
+__all__ = [
+    "StreamPartition",
+    "PingPongBuffer",
+    "CompressResult",
+    "run_serial_compress",
+    "run_pipelined_compress",
+    "run_parallel_decompress",
+    "throughput_report",
+]
+
+
+@dataclass(frozen=True)
+class StreamPartition:
+    """Flat bytes <-> (n_streams, stream_length) grid (pipeline.py:35-64).
+
+    Stream k covers bytes [k*L, (k+1)*L); the last stream is zero padded.
+    """
+
+    original_length: int
+    n_streams: int
+    stream_length: int
+
+    @classmethod
+    def from_length(cls, length: int, n_streams: int) -> "StreamPartition":
+        return cls(length, n_streams, -(-length // n_streams) if length else 0)
+
+    @property
+    def pad(self) -> int:
+        return self.n_streams * self.stream_length - self.original_length
+
+    def split(self, data: bytes) -> np.ndarray:
+        if len(data) != self.original_length:
+            raise ValueError("data length does not match partition")
+        grid = np.zeros(self.n_streams * self.stream_length, dtype=np.uint8)
+        grid[:self.original_length] = np.frombuffer(data, dtype=np.uint8)
+        return grid.reshape(self.n_streams, self.stream_length)
+
+    def join(self, mat: np.ndarray) -> bytes:
+        return mat.reshape(-1)[:self.original_length].tobytes()
+
+
+_LEGAL = {("empty", "filling"), ("filling", "full"), ("full", "draining"), ("draining", "empty")}
+
+
+class PingPongBuffer:
+    """The two-slot handoff protocol of pipeline.py:67-149, host side.
+
+    The device executor implements this protocol with CUDA events (model
+    stream records "full" after the head kernel writes slot i%2; the coder
+    stream waits on it, encodes, and records "empty").  This class keeps the
+    reference's host API so a host-thread producer/consumer can still use it,
+    and it replays the device schedule into a ``trace`` callback.
+    """
+
+    def __init__(self, trace=None):
+        self._states = ["empty", "empty"]
+        self._cond = threading.Condition()
+        self._trace = trace
+        self._exc: BaseException | None = None
+        self._payload: list = [None, None]
+
+    def _set(self, slot: int, new: str) -> None:
+        old = self._states[slot]
+        assert (old, new) in _LEGAL, f"illegal slot transition {old} -> {new}"
+        self._states[slot] = new
+        if self._trace is not None:
+            self._trace((slot, old, new))
+
+    def _wait(self, slot: int, state: str) -> None:
+        with self._cond:
+            while self._states[slot] != state:
+                if self._exc is not None:
+                    raise self._exc
+                self._cond.wait(timeout=0.1)
+
+    def acquire_fill(self, step: int) -> int:
+        slot = step % 2
+        self._wait(slot, "empty")
+        with self._cond:
+            self._set(slot, "filling")
+        return slot
+
+    def commit_fill(self, slot: int, payload=None) -> None:
+        with self._cond:
+            self._payload[slot] = payload
+            self._set(slot, "full")
+            self._cond.notify_all()
+
+    def acquire_drain(self, step: int) -> int:
+        slot = step % 2
+        self._wait(slot, "full")
+        with self._cond:
+            self._set(slot, "draining")
+        return slot
+
+    def commit_drain(self, slot: int) -> None:
+        with self._cond:
+            self._payload[slot] = None
+            self._set(slot, "empty")
+            self._cond.notify_all()
+
+    def payload(self, slot: int):
+        return self._payload[slot]
+
+    def abort(self, exc: BaseException) -> None:
+        with self._cond:
+            if self._exc is None:
+                self._exc = exc
+            self._cond.notify_all()
+
+    def replay(self, steps: int) -> None:
+        """Emit the device schedule's slot transitions for ``steps`` timesteps."""
+        for i in range(steps):
+            s = self.acquire_fill(i)
+            self.commit_fill(s)
+            s = self.acquire_drain(i)
+            self.commit_drain(s)
+
+
+@dataclass
+class CompressResult:
+    streams: list
+    cfg: ModelConfig
+    partition: StreamPartition
+    losses: list = field(default_factory=list)
+    elapsed: float = 0.0
+    metrics: list | None = None
+
+
+def _metrics(phase: str, first_step: int, losses, elapsed: float, bytes_per_step: int) -> list:
+    """Per-step records of the --metrics tape (pipeline.py:162-185).
+
+    Losses come from the device; the per-step wall clock is the device run's
+    elapsed time spread uniformly (the graph replay has no host-visible steps).
+    """
+    n = len(losses)
+    recs = []
+    for k, loss in enumerate(losses):
+        el = elapsed * (k + 1) / max(n, 1)
+        recs.append({"phase": phase, "step": first_step + k, "loss_nats": float(loss),
+                     "bits_per_byte": float(loss) / LN2, "elapsed_s": el,
+                     "kb_per_min": ((first_step + k + 1) * bytes_per_step / 1024.0)
+                     / max(el / 60.0, 1e-9)})
+    return recs
+
+
+def _prepare(data: bytes, cfg: ModelConfig):
+    cfg = cfg.shrink_to_fit(len(data))
+    cfg.validate()
+    part = StreamPartition.from_length(len(data), cfg.batch)
+    mat = part.split(data)
+    warm = min(cfg.ctx_len, part.stream_length)
+    return cfg, part, mat, warm
+
+
+def _raise_device(status: int, err: _native.FadeError, what: str):
+    if status == 3:
+        raise CorruptionError(int(err.stream), int(err.step), _native.last_error())
+    if status == 4:
+        raise ModelDivergenceError(int(err.step), _native.last_error())
+    if status == 5:
+        raise ValueError(f"row {int(err.stream)} does not sum to 1 within quantizer tolerance")
+    raise RuntimeError(f"{what} failed (status {status}): {_native.last_error()}")
+
+
+def _compress(data: bytes, cfg: ModelConfig, variant: str, pipelined: bool,
+              collect_metrics: bool, trace=None) -> CompressResult:
+    t0 = time.perf_counter()
+    if not data:
+        return CompressResult([], cfg, StreamPartition.from_length(0, cfg.batch))
+    cfg, part, mat, warm = _prepare(data, cfg)
+    steps = part.stream_length
+    model = Predictor(cfg, variant) if steps > warm else None
+    if model is None:
+        _native.require_device()
+    lib = _native.lib()
+    lengths = np.zeros(cfg.batch, dtype=np.int64)
+    nsteps = steps - warm
+    losses = np.zeros(max(nsteps, 1), dtype=np.float64)
+    coder = ctypes.c_void_p()
+    err = _native.FadeError()
+    mat = np.ascontiguousarray(mat)
+    st = lib.fade_compress(model.handle if model else None, cfg.batch, mat.ctypes.data, steps,
+                           warm, 0, 1 if pipelined else 0, lengths.ctypes.data, losses.ctypes.data,
+                           None, ctypes.byref(coder), ctypes.byref(err))
+    if st != 0:
+        _raise_device(st, err, "fade_compress")
+    try:
+        payload = np.empty(int(lengths.sum()), dtype=np.uint8)
+        _native.check(lib.fade_coder_fetch(coder, payload.ctypes.data, payload.size),
+                      "fade_coder_fetch")
+    finally:
+        lib.fade_coder_destroy(coder)
+    offs = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    streams = [payload[offs[k]:offs[k + 1]].tobytes() for k in range(cfg.batch)]
+    loss_list = [float(x) for x in losses[:nsteps]] if nsteps > 0 else []
+    elapsed = time.perf_counter() - t0
+    if trace is not None:
+        PingPongBuffer(trace).replay(steps)
+    metrics = (_metrics("compress", warm, loss_list, elapsed, cfg.batch)
+               if collect_metrics else None)
+    return CompressResult(streams, cfg, part, loss_list, elapsed, metrics)
+
+
+def run_serial_compress(data: bytes, cfg: ModelConfig, variant: str = "full",
+                        coder_delay: float = 0.0, collect_metrics: bool = False) -> CompressResult:
+    """predict -> quantise -> encode -> train per step, one CUDA stream (pipeline.py:197-226).
+
+    ``coder_delay`` (the reference's latency injection) has no device analogue
+    and is accepted for API compatibility only.
+    """
+    return _compress(data, cfg, variant, False, collect_metrics)
+
+
+def run_pipelined_compress(data: bytes, cfg: ModelConfig, variant: str = "full",
+                           coder_delay: float = 0.0, collect_metrics: bool = False,
+                           trace=None) -> CompressResult:
+    """CSPP: coder stream double-buffered against the model stream (pipeline.py:229-299)."""
+    return _compress(data, cfg, variant, True, collect_metrics, trace)
+
+
+def clamp_workers(workers: int, n_streams: int) -> int:
+    """Largest worker count <= requested that divides the stream count (pipeline.py:302-307)."""
+    w = max(1, min(int(workers), n_streams))
+    while n_streams % w:
+        w -= 1
+    return w
+
+
+def run_parallel_decompress(payload: np.ndarray, offsets: np.ndarray, lengths: np.ndarray,
+                            cfg: ModelConfig, original_length: int, workers: int = 1,
+                            decode_delay: float = 0.0, want_losses: bool = False,
+                            collect_metrics: bool = False):
+    """Decode every stream while replaying the encoder's updates (pipeline.py:310-396).
+
+    One lane per stream replaces the reference's worker threads and their two
+    barriers per step; ``workers`` is accepted and clamped for API parity.
+    """
+    if original_length == 0:
+        return (b"", []) if want_losses else b""
+    t0 = time.perf_counter()
+    clamp_workers(workers, cfg.batch)
+    part = StreamPartition.from_length(original_length, cfg.batch)
+    steps = part.stream_length
+    warm = min(cfg.ctx_len, steps)
+    model = Predictor(cfg) if steps > warm else None
+    if model is None:
+        _native.require_device()
+    pay = np.asarray(payload, dtype=np.uint8)
+    offsets = np.asarray(offsets, dtype=np.int64)
+    lengths = np.ascontiguousarray(np.asarray(lengths, dtype=np.int64))
+    # the device decoder takes streams back to back; regather if they are not
+    std = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+    if not np.array_equal(offsets, std) or pay.size != int(lengths.sum()):
+        pay = np.concatenate([pay[o:o + n] for o, n in zip(offsets, lengths)]) \
+            if len(lengths) else pay[:0]
+    pay = np.ascontiguousarray(pay)
+    out = np.zeros((cfg.batch, steps), dtype=np.uint8)
+    nsteps = steps - warm
+    losses = np.zeros(max(nsteps, 1), dtype=np.float64)
+    err = _native.FadeError()
+    st = _native.lib().fade_decompress(model.handle if model else None, cfg.batch,
+                                       pay.ctypes.data if pay.size else None, pay.size,
+                                       lengths.ctypes.data, steps, warm, out.ctypes.data,
+                                       losses.ctypes.data, ctypes.byref(err))
+    if st != 0:
+        _raise_device(st, err, "fade_decompress")
+    data = part.join(out)
+    loss_list = [float(x) for x in losses[:nsteps]] if nsteps > 0 else []
+    if want_losses:
+        return data, loss_list
+    if collect_metrics:
+        return data, _metrics("decompress", warm, loss_list, time.perf_counter() - t0, cfg.batch)
+    return data
+
+
+def throughput_report(n_bytes: int, compress_s: float, decompress_s: float) -> dict:
+    """KB/min; the total is the harmonic 2*size over the summed time (pipeline.py:399-411)."""
+    kb = n_bytes / 1024.0
+    return {
+        "n_bytes": n_bytes,
+        "compress_s": compress_s,
+        "decompress_s": decompress_s,
+        "compress_kb_min": kb / max(compress_s / 60.0, 1e-12),
+        "decompress_kb_min": kb / max(decompress_s / 60.0, 1e-12),
+        "total_kb_min": 2.0 * kb / max((compress_s + decompress_s) / 60.0, 1e-12),
+    }

@@ -133,6 +133,47 @@ class TestModelOracle:
             assert hashlib.sha256(p[k].tobytes()).hexdigest() == dig[k], k
 
 
+def _tf32(a, mode):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    if mode == "rne":
+        u = u + 0xFFF + ((u >> 13) & 1)
+    return (u & 0xFFFFE000).astype(np.uint32).view(np.float32)
+
+
+class _TF32(np.ndarray):
+    mode = "trunc"
+
+    def __matmul__(self, other):
+        return np.matmul(_tf32(np.asarray(self), _TF32.mode), _tf32(np.asarray(other), _TF32.mode))
+
+    def __rmatmul__(self, other):
+        return np.matmul(_tf32(np.asarray(other), _TF32.mode), _tf32(np.asarray(self), _TF32.mode))
+
+
+@pytest.mark.parametrize("name", ["tiny", "mid"])
+def test_tf32_truncation_budget(name):
+    """The GPU gate in test_gpu_model.py is derived here: emulate TF32 operand
+    truncation (what tcgen05.kind::tf32 does) on the golden state and measure
+    the probability error against the reference."""
+    cfg, st, z = model_golden(name)
+    out = {}
+    for mode in ("trunc", "rne"):
+        m = OracleModel(cfg)
+        m.load_state(st)
+        _TF32.mode = mode
+        for k in list(m.p):
+            m.p[k] = m.p[k].view(_TF32)
+        m.cache = m.cache.view(_TF32)
+        lg, _ = m.forward(z["ctx"])
+        p = softmax64(np.asarray(lg))
+        ref = z["next_probs"]
+        kl = float(np.mean(np.sum(ref * (np.log2(ref) - np.log2(p)), axis=1)))
+        out[mode] = (float(np.abs(p - ref).max()), kl)
+    assert out["trunc"][0] < 1e-3 and out["trunc"][1] < 1e-5
+    assert out["rne"][1] < out["trunc"][1]
+
+
 def test_softmax_xent_grad_is_p_minus_onehot():
     rng = np.random.default_rng(0)
     lg = rng.normal(size=(8, 256)).astype(np.float32)

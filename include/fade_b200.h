@@ -151,6 +151,18 @@ FADE_API int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload,
 
 /* ---- measurement hooks (bench.py) ------------------------------------------ */
 
+/* The model's launch stream (cudaStream_t), so callers can time on it. */
+FADE_API int fade_model_stream(fade_model_t* m, void** stream);
+
+/* Time `iters` back-to-back launches of one step component in isolation on the
+ * model stream (state from the last step): 0 = FNR expand GEMM (e12, GeGLU
+ * epilogue), 1 = W12 gradient GEMM with fused Adam, 2 = W_mem gradient + Adam
+ * group, 3 = per-stream memory backward + Adam (bmm_bwd), 4 = FNR project GEMM
+ * (split-K).  Writes the mean ms per launch and the algorithmic bytes and
+ * FLOPs of one launch. */
+FADE_API int fade_bench_probe(fade_model_t* m, int which, int iters, double* ms, double* bytes,
+                              double* flops);
+
 /* Run `steps` model timesteps of compression starting at column `start` of a
  * device-resident B x L matrix, without host synchronisation; the coder keeps
  * its state in `coder` (created on first use).  Returns the number of kernel

@@ -1033,6 +1033,66 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
   return status;
 }
 
+int fade_model_stream(fade_model_t* m, void** stream) {
+  *stream = (void*)m->s_main;
+  return FADE_OK;
+}
+
+int fade_bench_probe(fade_model_t* m, int which, int iters, double* ms, double* bytes,
+                     double* flops) {
+  CK(cudaSetDevice(m->device));
+  const Dims& d = m->d;
+  const double B = d.B, H = d.H, Ep = d.Ep, C = d.C, X = d.X;
+  auto launch = [&]() -> int {
+    switch (which) {
+      case 0: return run_gemm(m, G_E12, m->s_main);
+      case 1: return run_gemm(m, G_W12, m->s_main);
+      case 2: return run_gemm(m, G_WROUTE_WMEM, m->s_main);
+      case 3: launch_bmm_bwd(m->M, 0, m->s_main); return FADE_OK;
+      case 4: return run_gemm(m, G_F, m->s_main);
+    }
+    set_last_error("bench_probe: unknown component");
+    return FADE_ERR_USAGE;
+  };
+  // algorithmic work of one launch (SURVEY.md section 8d accounting)
+  switch (which) {
+    case 0:   // z2[B,H] . W12[H,2Ep]: read W12 + z2, write a12 + wide
+      *flops = 2.0 * B * H * 2 * Ep;
+      *bytes = 4.0 * (H * 2 * Ep + B * H + B * 2 * Ep + B * Ep);
+      break;
+    case 1:   // dW12 = z2^T dA12 with Adam: p, m, v read + written (24 B/param)
+      *flops = 2.0 * H * 2 * Ep * B;
+      *bytes = 24.0 * H * 2 * Ep + 4.0 * (B * H + B * 2 * Ep);
+      break;
+    case 2:   // dW_route + dW_mem with Adam
+      *flops = 2.0 * (H * H + C * H) * B;
+      *bytes = 24.0 * (H * H + C * H) + 4.0 * (B * H * 2 + B * C + B * H);
+      break;
+    case 3:   // per-stream W_U: p, m, v read + written
+      *flops = 4.0 * B * X * X;
+      *bytes = 24.0 * B * X * X + 4.0 * 3 * B * X;
+      break;
+    case 4:   // wide[B,E] . W_f[E,H] split-K partials
+      *flops = 2.0 * B * d.E * H;
+      *bytes = 4.0 * (d.E * H + B * Ep + (double)m->M.splits_f * B * H);
+      break;
+  }
+  TRY(launch());   // warm
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, m->s_main));
+  for (int i = 0; i < iters; ++i) TRY(launch());
+  CK(cudaEventRecord(e1, m->s_main));
+  CK(cudaEventSynchronize(e1));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = t / iters;
+  return FADE_OK;
+}
+
 int fade_bench_compress_steps(fade_model_t* m, const uint8_t* data_dev, int64_t L, int64_t start,
                               int64_t steps, fade_coder_t** coder, int* launches, void* stream) {
   (void)stream;

@@ -71,7 +71,8 @@ struct fade_model {
   void* mem = nullptr;
   ModelPtrs M;
   StepState* st = nullptr;      // device
-  GemmParams G[G_COUNT];
+  GemmParams G[G_COUNT];        // step schedule (Adam fused into dW epilogues)
+  GemmParams Gg[G_COUNT];       // loss_grads variant (dW epilogues store gradients)
   int bn[G_COUNT];
   uint8_t* ctx_buf = nullptr;   // [B][T]  (predict API)
   uint8_t* tgt_buf = nullptr;   // [B]
@@ -180,18 +181,20 @@ static GemmDesc gd(const float* A, long long lda, int at, const float* B, long l
   return g;
 }
 
-static int build_gemms(fade_model* m) {
+// grad_only = true builds the loss_grads variant: weight-gradient GEMMs store
+// the raw gradient into the g buffers instead of applying Adam.
+static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   const Dims& d = m->d;
   ModelPtrs& M = m->M;
   Acts& a = M.a;
   const int B = d.B, H = d.H, X = d.X, E = d.E, Ep = d.Ep, C = d.C;
   for (int i = 0; i < G_COUNT; ++i) {
-    memset(&m->G[i], 0, sizeof(GemmParams));
+    memset(&Gs[i], 0, sizeof(GemmParams));
     m->bn[i] = 64;
-    m->G[i].adam = &m->st->adam;
+    Gs[i].adam = &m->st->adam;
   }
   m->bn[G_E12] = 128;
-  auto b = [&](int id) { return Builder{&m->G[id], m->bn[id]}; };
+  auto b = [&](int id) { return Builder{&Gs[id], m->bn[id]}; };
   Tensor4* w = M.w;
   // forward
   {
@@ -199,7 +202,6 @@ static int build_gemms(fade_model* m) {
     TRY(bl.add(gd(a.x, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, a.rpre, H)));
     GemmDesc g = gd(a.cache, C, 0, w[P_W_MEM].p, H, 0, B, H, C, EPI_STORE, a.ws_mem, H);
     g.splits = M.splits_mem;
-    g.c_split = (long long)B * H;
     TRY(bl.add(g));
   }
   TRY(b(G_DOWN).add(gd(a.z, H, 0, w[P_W_DOWN].p, X, 0, B, X, H, EPI_STORE, a.zd, X)));
@@ -212,12 +214,12 @@ static int build_gemms(fade_model* m) {
     GemmDesc g = gd(a.z2, H, 0, w[P_W_E1].p, 2LL * Ep, 0, B, 2 * Ep, H, EPI_GEGLU, a.a12, 2LL * Ep);
     g.aux0 = a.wide;
     g.ld_aux = Ep;
+    g.aux_cols = Ep;
     TRY(b(G_E12).add(g));
   }
   {
     GemmDesc g = gd(a.wide, Ep, 0, w[P_W_F].p, H, 0, B, H, E, EPI_STORE, a.ws_f, H);
     g.splits = M.splits_f;
-    g.c_split = (long long)B * H;
     TRY(b(G_F).add(g));
   }
   {
@@ -231,16 +233,17 @@ static int build_gemms(fade_model* m) {
     GemmDesc g = gd(a.dnpre, H, 0, w[P_W_F].p, H, 1, B, E, H, EPI_GEGLU_BWD, a.da12, 2LL * Ep);
     g.aux1 = a.a12;
     g.ld_aux = 2LL * Ep;
+    g.c_cols = 2LL * Ep;
+    g.aux_cols = 2LL * Ep;
     // W_f has E rows; rows [E, Ep) read as zeros through the TMA bounds, and the
     // tiles cover whole 64-column interleave blocks of dA12
     TRY(b(G_DWIDE).add(g));
-    m->G[G_DWIDE].prob[0].N = Ep;
-    m->G[G_DWIDE].prob[0].tiles_n = cdiv(Ep, 64);
+    Gs[G_DWIDE].prob[0].N = Ep;
+    Gs[G_DWIDE].prob[0].tiles_n = cdiv(Ep, 64);
   }
   {
     GemmDesc g = gd(a.da12, 2LL * Ep, 0, w[P_W_E1].p, 2LL * Ep, 1, B, H, 2 * Ep, EPI_STORE, a.ws_dz2, H);
     g.splits = M.splits_dz2;
-    g.c_split = (long long)B * H;
     TRY(b(G_DZ2).add(g));
   }
   {
@@ -257,9 +260,14 @@ static int build_gemms(fade_model* m) {
   }
   // weight gradients with the Adam step fused into the epilogue
   auto adam = [&](GemmDesc g, const Tensor4& t) {
-    g.C = t.p;
-    g.aux0 = t.m;
-    g.aux2 = t.v;
+    if (grad_only) {
+      g.epi = EPI_GRAD;
+      g.C = t.g;
+    } else {
+      g.C = t.p;
+      g.aux0 = t.m;
+      g.aux2 = t.v;
+    }
     return g;
   };
   TRY(b(G_WHEAD).add(adam(gd(a.h, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD])));
@@ -280,21 +288,7 @@ static int build_gemms(fade_model* m) {
 }
 
 static int run_gemm(fade_model* m, int id, cudaStream_t s, bool grad_only = false) {
-  GemmParams G = m->G[id];
-  if (grad_only) {
-    for (int q = 0; q < G.nprob; ++q) {
-      GemmProblem& P = G.prob[q];
-      if (P.epi != EPI_ADAM) continue;
-      // the gradient buffer sits at the same offset in the g arena as C in p
-      for (int i = 0; i < P_COUNT; ++i)
-        if (m->M.w[i].p == P.C) {
-          P.C = m->M.w[i].g;
-          break;
-        }
-      P.epi = EPI_GRAD;
-    }
-  }
-  return gemm_launch(G, m->bn[id], s);
+  return gemm_launch(grad_only ? m->Gg[id] : m->G[id], m->bn[id], s);
 }
 
 static int allocate(fade_model* m) {
@@ -309,7 +303,7 @@ static int allocate(fade_model* m) {
   M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
   M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
   M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
-  M.emb_chunk = 16;
+  M.emb_chunk = 4;
 
   struct Item { void** ptr; size_t bytes; };
   std::vector<Item> items;
@@ -529,7 +523,8 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   CK(cudaEventCreateWithFlags(&m->ev_side_done, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&m->ev_coder_join, cudaEventDisableTiming));
   TRY(allocate(m.get()));
-  TRY(build_gemms(m.get()));
+  TRY(build_gemms(m.get(), m->G, false));
+  TRY(build_gemms(m.get(), m->Gg, true));
   *out = m.release();
   return FADE_OK;
 }

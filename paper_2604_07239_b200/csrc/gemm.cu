@@ -61,6 +61,24 @@ int make_tmap_mnmajor(CUtensorMap* map, const float* ptr, long long mn, long lon
   return encode(map, ptr, mn, k, ld, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
+// split-K workspace [slices][rows][cols] (slice stride rows*ld): 32 x 128 x 1 boxes
+static int make_tmap_slices(CUtensorMap* map, const float* ptr, long long rows, long long cols,
+                            long long ld, int slices) {
+  if (int s = get_encoder()) return s;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)slices};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(rows * ld * 4)};
+  cuuint32_t box[3] = {32, (cuuint32_t)kBM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)ptr, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled (split-K slices) failed");
+    return FADE_ERR_CUDA;
+  }
+  return FADE_OK;
+}
+
 int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   memset(P, 0, sizeof(*P));
   P->M = d.M;
@@ -84,19 +102,39 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   P->tiles_m = cdiv(d.M, kBM);
   P->tiles_n = cdiv(d.N, BN);
   P->epi = d.epi;
-  P->C = d.C;
-  P->ldc = d.ldc;
-  P->c_split = d.c_split;
   P->bias = d.bias;
-  P->aux0 = d.aux0;
-  P->aux1 = d.aux1;
-  P->aux2 = d.aux2;
-  P->ld_aux = d.ld_aux;
   if (P->splits > 1 && d.epi != EPI_STORE) {
     set_last_error("split-K is only valid with the partial-store epilogue");
     return FADE_ERR_USAGE;
   }
-  return FADE_OK;
+  // output / aux tile maps (row-major, 32 x 128 boxes, 128B swizzle)
+  const long long crow = d.c_rows ? d.c_rows : d.M, ccol = d.c_cols ? d.c_cols : d.N;
+  const long long arow = d.aux_rows ? d.aux_rows : crow, acol = d.aux_cols ? d.aux_cols : ccol;
+  P->c_rows = (int)crow;
+  auto tile_map = [](CUtensorMap* m, const float* p, long long rows, long long cols, long long ld) {
+    return make_tmap_kmajor(m, p, rows, cols, ld, kBM);
+  };
+  switch (d.epi) {
+    case EPI_STORE:
+    case EPI_GRAD:
+      s = P->splits > 1 ? make_tmap_slices(&P->tc, d.C, crow, ccol, d.ldc, P->splits)
+                        : tile_map(&P->tc, d.C, crow, ccol, d.ldc);
+      break;
+    case EPI_ADAM:
+      s = tile_map(&P->tc, d.C, crow, ccol, d.ldc);
+      if (!s) s = tile_map(&P->tx0, d.aux0, crow, ccol, d.ldc);
+      if (!s) s = tile_map(&P->tx2, d.aux2, crow, ccol, d.ldc);
+      break;
+    case EPI_GEGLU:
+      s = tile_map(&P->tc, d.C, crow, ccol, d.ldc);
+      if (!s) s = tile_map(&P->tx0, d.aux0, arow, acol, d.ld_aux);
+      break;
+    case EPI_GEGLU_BWD:
+      s = tile_map(&P->tc, d.C, crow, ccol, d.ldc);
+      if (!s) s = tile_map(&P->tx1, d.aux1, arow, acol, d.ld_aux);
+      break;
+  }
+  return s;
 }
 
 template <int BN>

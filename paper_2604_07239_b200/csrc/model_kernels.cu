@@ -559,20 +559,36 @@ __global__ void __launch_bounds__(kRowThreads) k_bmm_bwd(ModelPtrs M, int grad_o
   }
   __syncthreads();
   const long long base = (long long)b * X * X;
-  float* Wp = M.w[P_W_MIX].p + base;
-  float* Wm = M.w[P_W_MIX].m + base;
-  float* Wv = M.w[P_W_MIX].v + base;
-  float* Wg = M.w[P_W_MIX].g + base;
+  float4* __restrict__ Wp = (float4*)(M.w[P_W_MIX].p + base);
+  float4* __restrict__ Wm = (float4*)(M.w[P_W_MIX].m + base);
+  float4* __restrict__ Wv = (float4*)(M.w[P_W_MIX].v + base);
+  float4* __restrict__ Wg = (float4*)(M.w[P_W_MIX].g + base);
   const AdamScalars a = M.st->adam;
+  const int X4 = X / 4;      // X is a multiple of 4 (ModelConfig.device_check)
+  // one warp per row i; lanes cover 4 consecutive columns each (float4), so
+  // the read-modify-write of p, m, v is one coalesced 512-byte pass per row
+#pragma unroll 2
   for (int i = w; i < X; i += kRowThreads / 32) {
     float acc = 0.f;
-    for (int j = lane; j < X; j += 32) {
-      const long long q = (long long)i * X + j;
-      const float wv = Wp[q];
-      acc += dus[j] * wv;
-      const float g = zds[i] * dus[j];
-      if (grad_only) Wg[q] = g;
-      else adam_update(a, g, Wp + q, Wm + q, Wv + q);
+    const float zi = zds[i];
+    for (int j4 = lane; j4 < X4; j4 += 32) {
+      const long long q = (long long)i * X4 + j4;
+      float4 p = Wp[q];
+      const float4 du4 = *(const float4*)(dus + 4 * j4);
+      acc += du4.x * p.x + du4.y * p.y + du4.z * p.z + du4.w * p.w;
+      const float4 g = make_float4(zi * du4.x, zi * du4.y, zi * du4.z, zi * du4.w);
+      if (grad_only) {
+        Wg[q] = g;
+      } else {
+        float4 m = Wm[q], v = Wv[q];
+        adam_update(a, g.x, &p.x, &m.x, &v.x);
+        adam_update(a, g.y, &p.y, &m.y, &v.y);
+        adam_update(a, g.z, &p.z, &m.z, &v.z);
+        adam_update(a, g.w, &p.w, &m.w, &v.w);
+        Wp[q] = p;
+        Wm[q] = m;
+        Wv[q] = v;
+      }
     }
     acc = warp_sum(acc);
     if (lane == 0) M.a.dzd[(long long)b * X + i] = acc;
@@ -645,7 +661,12 @@ __global__ void __launch_bounds__(kRowThreads) k_trunk_bwd(ModelPtrs M, const ui
   float* rr = M.a.rowred + (long long)b * M.sl.rowred;
   const float* Wg = M.w[P_W_GATE].p;
   const float* Wv = M.w[P_W_VAL].p;
-  for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) ck[j] = M.w[P_CONV_K].p[j];
+  // taps transposed to [tap][co][ci] so the input-gradient loop below reads
+  // consecutive ci across lanes (no 32-way bank conflict)
+  for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) {
+    const int tap = j / (d.D * d.D), ci = (j / d.D) % d.D, co = j % d.D;
+    ck[(tap * d.D + co) * d.D + ci] = M.w[P_CONV_K].p[j];
+  }
   for (int o = tid; o < d.D; o += blockDim.x) {
     const float gp = M.a.gpre[(long long)b * d.D + o];
     const float vp = M.a.vpre[(long long)b * d.D + o];
@@ -709,7 +730,7 @@ __global__ void __launch_bounds__(kRowThreads) k_trunk_bwd(ModelPtrs M, const ui
       const int t = sidx - tap + pad;
       if (t < 0 || t >= d.T) continue;
       float part = 0.f;
-      for (int co = 0; co < d.D; ++co) part += dcv[t * d.D + co] * ck[(tap * d.D + ci) * d.D + co];
+      for (int co = 0; co < d.D; ++co) part += dcv[t * d.D + co] * ck[(tap * d.D + co) * d.D + ci];
       acc += part;
     }
     dls[j] = acc;

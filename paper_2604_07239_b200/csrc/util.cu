@@ -38,7 +38,7 @@ int fade_debug_gemm(const float* A, long long lda, int a_trans, const float* B, 
   d.M = M; d.N = N; d.K = K;
   d.splits = splits;
   d.epi = EPI_STORE;
-  d.C = C; d.ldc = ldc; d.c_split = (long long)M * ldc;
+  d.C = C; d.ldc = ldc;
   if (int s = gemm_setup(&G.prob[0], d, bn)) return s;
   G.nprob = 1;
   return gemm_launch(G, bn, (cudaStream_t)stream);

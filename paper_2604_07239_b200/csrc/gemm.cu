@@ -137,31 +137,37 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   return s;
 }
 
-template <int BN>
-static int launch_bn(GemmParams& G, cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
+template <int BN, int ET>
+static int launch_cfg(GemmParams& G, cudaStream_t st) {
+  using Cfg = GemmCfg<BN, ET>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN, ET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::kSmem);
   });
   FADE_CUDA_TRY(attr_err);
-  k_gemm_tf32<BN><<<G.total_tiles, kGemmThreads, Cfg::kSmem, st>>>(G);
+  FADE_CUDA_TRY(launch_pdl(k_gemm_tf32<BN, ET>, dim3(G.total_tiles), dim3(kGemmThreads),
+                           (size_t)Cfg::kSmem, st, G));
   FADE_CUDA_TRY(cudaGetLastError());
   return FADE_OK;
 }
 
 int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
-  int t = 0;
+  int t = 0, et = 1;
   for (int q = 0; q < G.nprob; ++q) {
     G.prob[q].tile_begin = t;
     t += G.prob[q].tiles_m * G.prob[q].tiles_n * G.prob[q].splits;
+    et = std::max(et, epi_tiles(G.prob[q].epi, BN));
   }
   G.total_tiles = t;
   if (t == 0) return FADE_OK;
-  if (BN == 64) return launch_bn<64>(G, st);
-  if (BN == 128) return launch_bn<128>(G, st);
-  set_last_error("unsupported GEMM tile width");
+  if (BN == 64 && et == 1) return launch_cfg<64, 1>(G, st);
+  if (BN == 64 && et == 2) return launch_cfg<64, 2>(G, st);
+  if (BN == 64 && et == 3) return launch_cfg<64, 3>(G, st);
+  if (BN == 128 && et == 2) return launch_cfg<128, 2>(G, st);
+  if (BN == 128 && et == 3) return launch_cfg<128, 3>(G, st);
+  set_last_error("unsupported GEMM tile configuration");
   return FADE_ERR_USAGE;
 }
 

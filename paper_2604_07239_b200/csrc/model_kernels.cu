@@ -47,6 +47,7 @@ __device__ __forceinline__ void ln_bwd_means(const float* gs, const float* xhat_
 // trunk + local stream forward (model.py:118-137)
 __global__ void __launch_bounds__(kRowThreads) k_trunk_fwd(ModelPtrs M, const uint8_t* src,
                                                            long long ld_src, int use_col) {
+  pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
@@ -177,12 +178,13 @@ void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (3 * d.H + (2 + d.K) * d.D * d.D + d.D + 2 * d.T + 32) +
                       sizeof(int) * d.T;
-  k_trunk_fwd<<<d.B, kRowThreads, smem, s>>>(M, src, ld_src, use_col);
+  launch_pdl(k_trunk_fwd, dim3(d.B), dim3(kRowThreads), smem, s, M, src, ld_src, use_col);
 }
 
 // ---------------------------------------------------------------------------
 // global stream finish + router + mixer LayerNorm (model.py:128-153)
 __global__ void __launch_bounds__(kRowThreads) k_mix_fwd(ModelPtrs M) {
+  pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
@@ -236,11 +238,12 @@ __global__ void __launch_bounds__(kRowThreads) k_mix_fwd(ModelPtrs M) {
 }
 
 void launch_mix_fwd(const ModelPtrs& M, cudaStream_t s) {
-  k_mix_fwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+  launch_pdl(k_mix_fwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // per-stream persistent memory: u[b] = zd[b] @ W_U[b]  (ops.py:44-54)
 __global__ void __launch_bounds__(kRowThreads) k_bmm_fwd(ModelPtrs M) {
+  pdl_enter();
   const int X = M.d.X, b = blockIdx.x;
   extern __shared__ float zs[];
   for (int i = threadIdx.x; i < X; i += blockDim.x) zs[i] = M.a.zd[(long long)b * X + i];
@@ -254,11 +257,12 @@ __global__ void __launch_bounds__(kRowThreads) k_bmm_fwd(ModelPtrs M) {
 }
 
 void launch_bmm_fwd(const ModelPtrs& M, cudaStream_t s) {
-  k_bmm_fwd<<<M.d.B, kRowThreads, sizeof(float) * M.d.X, s>>>(M);
+  launch_pdl(k_bmm_fwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * M.d.X, s, M);
 }
 
 // self-gated coarse refiner + FNR LayerNorm (model.py:156-167)
 __global__ void __launch_bounds__(kRowThreads) k_coarse_fwd(ModelPtrs M) {
+  pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
@@ -287,11 +291,12 @@ __global__ void __launch_bounds__(kRowThreads) k_coarse_fwd(ModelPtrs M) {
 }
 
 void launch_coarse_fwd(const ModelPtrs& M, cudaStream_t s) {
-  k_coarse_fwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+  launch_pdl(k_coarse_fwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // FNR output: split-K reduce, LayerNorm, gelu, residual (model.py:170-172)
 __global__ void __launch_bounds__(kRowThreads) k_out_fwd(ModelPtrs M) {
+  pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(kRowThreads) k_out_fwd(ModelPtrs M) {
 }
 
 void launch_out_fwd(const ModelPtrs& M, cudaStream_t s) {
-  k_out_fwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+  launch_pdl(k_out_fwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // ---------------------------------------------------------------------------
@@ -350,6 +355,7 @@ __device__ __forceinline__ double block_sum_d256(double v, double* red) {
 }
 
 __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
+  pdl_enter();
   __shared__ QuantSmem qs;
   __shared__ double dred[8];
   __shared__ unsigned cum_s[kAlphabet + 1];
@@ -432,11 +438,12 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
 }
 
 void launch_head(const ModelPtrs& M, const HeadArgs& h, cudaStream_t s) {
-  k_head<<<M.d.B, 256, 0, s>>>(M, h);
+  launch_pdl(k_head, dim3(M.d.B), dim3(256), 0, s, M, h);
 }
 
 // Adam bias-correction scalars from the device step counter (optim.py:26-30)
 __global__ void k_adam_prep(StepState* st, double lr, double b1, double b2, double eps) {
+  pdl_enter();
   const long long t = ++st->adam_t;
   const double c1 = 1.0 - pow(b1, (double)t);
   const double c2 = 1.0 - pow(b2, (double)t);
@@ -453,7 +460,7 @@ __global__ void k_adam_prep(StepState* st, double lr, double b1, double b2, doub
 
 void launch_adam_prep(const ModelPtrs& M, double lr, double b1, double b2, double eps,
                       cudaStream_t s) {
-  k_adam_prep<<<1, 1, 0, s>>>(M.st, lr, b1, b2, eps);
+  launch_pdl(k_adam_prep, dim3(1), dim3(1), 0, s, M.st, lr, b1, b2, eps);
 }
 
 __device__ __forceinline__ void adam_update(const AdamScalars& a, float g, float* p, float* m,
@@ -473,6 +480,7 @@ __device__ __forceinline__ void adam_update(const AdamScalars& a, float g, float
 
 // h = gelu(LN(npre)) + lam_out * h_c   (model.py:170-172 backward)
 __global__ void __launch_bounds__(kRowThreads) k_out_bwd(ModelPtrs M) {
+  pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
@@ -503,11 +511,12 @@ __global__ void __launch_bounds__(kRowThreads) k_out_bwd(ModelPtrs M) {
 }
 
 void launch_out_bwd(const ModelPtrs& M, cudaStream_t s) {
-  k_out_bwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+  launch_pdl(k_out_bwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // z2 = LN(h_c); h_c = inner * sigmoid(cpre) + lam_mix * h_mix   (backward)
 __global__ void __launch_bounds__(kRowThreads) k_coarse_bwd(ModelPtrs M) {
+  pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
@@ -542,12 +551,13 @@ __global__ void __launch_bounds__(kRowThreads) k_coarse_bwd(ModelPtrs M) {
 }
 
 void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s) {
-  k_coarse_bwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+  launch_pdl(k_coarse_bwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // per-stream memory backward + its Adam step in one streaming pass
 // (ops.py:48-52 for the gradients, optim.py:25-44 for the update)
 __global__ void __launch_bounds__(kRowThreads) k_bmm_bwd(ModelPtrs M, int grad_only) {
+  pdl_enter();
   const int X = M.d.X, b = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   extern __shared__ float sm[];
@@ -596,11 +606,12 @@ __global__ void __launch_bounds__(kRowThreads) k_bmm_bwd(ModelPtrs M, int grad_o
 }
 
 void launch_bmm_bwd(const ModelPtrs& M, int grad_only, cudaStream_t s) {
-  k_bmm_bwd<<<M.d.B, kRowThreads, sizeof(float) * 2 * M.d.X, s>>>(M, grad_only);
+  launch_pdl(k_bmm_bwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * 2 * M.d.X, s, M, grad_only);
 }
 
 // mixer LayerNorm + router mix + global-stream gelu (model.py:128-153 backward)
 __global__ void __launch_bounds__(kRowThreads) k_mix_bwd(ModelPtrs M) {
+  pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
@@ -639,12 +650,13 @@ __global__ void __launch_bounds__(kRowThreads) k_mix_bwd(ModelPtrs M) {
 }
 
 void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s) {
-  k_mix_bwd<<<M.d.B, kRowThreads, sizeof(float) * (M.d.H + 32), s>>>(M);
+  launch_pdl(k_mix_bwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // trunk + local stream backward (model.py:118-137 backward)
 __global__ void __launch_bounds__(kRowThreads) k_trunk_bwd(ModelPtrs M, const uint8_t* src,
                                                            long long ld_src, int use_col) {
+  pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
@@ -772,7 +784,7 @@ void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
                       cudaStream_t s) {
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (4 * d.H + d.K * d.D * d.D + 3 * d.D + 32);
-  k_trunk_bwd<<<d.B, kRowThreads, smem, s>>>(M, src, ld_src, use_col);
+  launch_pdl(k_trunk_bwd, dim3(d.B), dim3(kRowThreads), smem, s, M, src, ld_src, use_col);
 }
 
 // Column sums of the per-row reduction buffer + dlogits (b_head), in a fixed
@@ -780,6 +792,7 @@ void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
 constexpr int kColWarps = 32;
 __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int grad_only,
                                                                double* losses) {
+  pdl_enter();
   __shared__ float part[kColWarps][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -810,12 +823,13 @@ __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int 
 
 void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, cudaStream_t s) {
   const int total = M.sl.rowred + kAlphabet;
-  k_small_adam<<<cdiv(total, 32), 32 * kColWarps, 0, s>>>(M, grad_only, losses);
+  launch_pdl(k_small_adam, dim3(cdiv(total, 32)), dim3(32 * kColWarps), 0, s, M, grad_only, losses);
 }
 
 // embedding gradient: deterministic two-level scatter-add (ops.py:234-243)
 __global__ void __launch_bounds__(256) k_emb_part(ModelPtrs M, const uint8_t* src,
                                                   long long ld_src, int use_col) {
+  pdl_enter();
   const Dims d = M.d;
   extern __shared__ float acc[];          // [256][D]
   const int chunk = blockIdx.x;
@@ -841,6 +855,7 @@ __global__ void __launch_bounds__(256) k_emb_part(ModelPtrs M, const uint8_t* sr
 }
 
 __global__ void k_emb_adam(ModelPtrs M, int nchunks, int grad_only) {
+  pdl_enter();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = kAlphabet * M.d.D;
   if (q >= n) return;
@@ -854,17 +869,18 @@ __global__ void k_emb_adam(ModelPtrs M, int nchunks, int grad_only) {
 void launch_emb_grad(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                      int grad_only, cudaStream_t s) {
   const int nchunks = cdiv(M.d.B, M.emb_chunk);
-  k_emb_part<<<nchunks, 256, sizeof(float) * kAlphabet * M.d.D, s>>>(M, src, ld_src, use_col);
-  k_emb_adam<<<cdiv(kAlphabet * M.d.D, 256), 256, 0, s>>>(M, nchunks, grad_only);
+  launch_pdl(k_emb_part, dim3(nchunks), dim3(256), sizeof(float) * kAlphabet * M.d.D, s, M, src, ld_src, use_col);
+  launch_pdl(k_emb_adam, dim3(cdiv(kAlphabet * M.d.D, 256)), dim3(256), 0, s, M, nchunks, grad_only);
 }
 
 __global__ void k_advance(StepState* st, int trained) {
+  pdl_enter();
   st->col += 1;
   st->step_count += trained;
 }
 
 void launch_advance(const ModelPtrs& M, int trained, cudaStream_t s) {
-  k_advance<<<1, 1, 0, s>>>(M.st, trained);
+  launch_pdl(k_advance, dim3(1), dim3(1), 0, s, M.st, trained);
 }
 
 }  // namespace fade

@@ -18,6 +18,7 @@ __device__ __forceinline__ void store_lane(const EncState& e, int b, const EncLa
 }
 
 __global__ void k_enc_init(EncState e, int B) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b == 0) {
     *e.col = 0;
@@ -28,11 +29,12 @@ __global__ void k_enc_init(EncState e, int B) {
 }
 
 void launch_enc_init(const EncState& e, int B, cudaStream_t s) {
-  k_enc_init<<<cdiv(B, kCoderThreads), kCoderThreads, 0, s>>>(e, B);
+  launch_pdl(k_enc_init, dim3(cdiv(B, kCoderThreads)), dim3(kCoderThreads), 0, s, e, B);
 }
 
 __global__ void k_encode_warm(EncState e, int B, const uint8_t* data, long long ld,
                               long long warm) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) {
     EncLane s = load_lane(e, b);
@@ -48,11 +50,12 @@ __global__ void k_encode_warm(EncState e, int B, const uint8_t* data, long long 
 
 void launch_encode_warm(const EncState& e, int B, const uint8_t* data, long long ld, long long warm,
                         cudaStream_t s) {
-  k_encode_warm<<<cdiv(B, kCoderThreads), kCoderThreads, 0, s>>>(e, B, data, ld, warm);
+  launch_pdl(k_encode_warm, dim3(cdiv(B, kCoderThreads)), dim3(kCoderThreads), 0, s, e, B, data, ld, warm);
 }
 
 __global__ void k_encode_col(EncState e, int B, const uint8_t* data, long long ld,
                              const unsigned* cum) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   const long long col = *e.col;
   if (b < B) {
@@ -77,10 +80,11 @@ __global__ void k_encode_col(EncState e, int B, const uint8_t* data, long long l
 
 void launch_encode_col(const EncState& e, int B, const uint8_t* data, long long ld,
                        const unsigned* cum, cudaStream_t s) {
-  k_encode_col<<<cdiv(B, kCoderThreads), kCoderThreads, 0, s>>>(e, B, data, ld, cum);
+  launch_pdl(k_encode_col, dim3(cdiv(B, kCoderThreads)), dim3(kCoderThreads), 0, s, e, B, data, ld, cum);
 }
 
 __global__ void k_encode_flush(EncState e, int B) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   EncLane s = load_lane(e, b);
@@ -89,10 +93,11 @@ __global__ void k_encode_flush(EncState e, int B) {
 }
 
 void launch_encode_flush(const EncState& e, int B, cudaStream_t s) {
-  k_encode_flush<<<cdiv(B, kCoderThreads), kCoderThreads, 0, s>>>(e, B);
+  launch_pdl(k_encode_flush, dim3(cdiv(B, kCoderThreads)), dim3(kCoderThreads), 0, s, e, B);
 }
 
 __global__ void k_compact(EncState e, const long long* off, uint8_t* out) {
+  pdl_enter();
   const int b = blockIdx.x;
   const long long n = e.blen[b];
   const uint8_t* src = e.buf + (long long)b * e.cap;
@@ -101,7 +106,7 @@ __global__ void k_compact(EncState e, const long long* off, uint8_t* out) {
 }
 
 void launch_compact(const EncState& e, int B, const long long* off, uint8_t* out, cudaStream_t s) {
-  k_compact<<<B, 256, 0, s>>>(e, off, out);
+  launch_pdl(k_compact, dim3(B), dim3(256), 0, s, e, off, out);
 }
 
 __device__ __forceinline__ void dec_error(unsigned long long* key, long long step, long long stream,
@@ -113,6 +118,7 @@ __device__ __forceinline__ void dec_error(unsigned long long* key, long long ste
 
 // kernels.py:186-197; a stream shorter than the 4-byte tail is corrupt (coder.py:117-118)
 __global__ void k_dec_prime(DecState d, int B, unsigned long long* err_key) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   if (d.dlen[b] < 4) {
@@ -131,7 +137,7 @@ __global__ void k_dec_prime(DecState d, int B, unsigned long long* err_key) {
 }
 
 void launch_dec_prime(const DecState& d, int B, unsigned long long* err_key, cudaStream_t s) {
-  k_dec_prime<<<cdiv(B, kCoderThreads), kCoderThreads, 0, s>>>(d, B, err_key);
+  launch_pdl(k_dec_prime, dim3(cdiv(B, kCoderThreads)), dim3(kCoderThreads), 0, s, d, B, err_key);
 }
 
 struct UniformCum {
@@ -140,6 +146,7 @@ struct UniformCum {
 
 __global__ void k_decode_warm(DecState d, int B, uint8_t* out, long long ld, long long warm,
                               unsigned long long* err_key) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   DecLane s{d.code[b], d.rng[b], d.pos[b]};
@@ -162,7 +169,7 @@ __global__ void k_decode_warm(DecState d, int B, uint8_t* out, long long ld, lon
 
 void launch_decode_warm(const DecState& d, int B, uint8_t* out, long long ld, long long warm,
                         unsigned long long* err_key, cudaStream_t s) {
-  k_decode_warm<<<cdiv(B, kCoderThreads), kCoderThreads, 0, s>>>(d, B, out, ld, warm, err_key);
+  launch_pdl(k_decode_warm, dim3(cdiv(B, kCoderThreads)), dim3(kCoderThreads), 0, s, d, B, out, ld, warm, err_key);
 }
 
 }  // namespace fade

@@ -1,0 +1,17 @@
+import ctypes, sys, os
+sys.path.insert(0, os.getcwd())
+import numpy as np, torch
+from paper_2604_07239_b200 import ModelConfig, _native, corpus
+from paper_2604_07239_b200.model import Predictor
+from paper_2604_07239_b200.pipeline import StreamPartition
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+cfg = ModelConfig(batch=512, workers=1)
+data = corpus.make_text(4_000_000, 12)
+part = StreamPartition.from_length(len(data), cfg.batch)
+mat = np.ascontiguousarray(part.split(data)); L = part.stream_length
+dmat = torch.from_numpy(mat).cuda()
+m = Predictor(cfg)
+lib = _native.lib(); coder = ctypes.c_void_p(); la = ctypes.c_int()
+_native.check(lib.fade_bench_compress_steps(m.handle, dmat.data_ptr(), L, 16, n, ctypes.byref(coder), ctypes.byref(la), None), "steps")
+torch.cuda.synchronize()
+print("launches per timestep", la.value)

@@ -151,8 +151,12 @@ static int small_offset(const SmallLayout& s, int i) {
   return -1;
 }
 
+constexpr int kWideBN = 256;
+
+// split-K count: as many slices as fit in ONE wave of 148 SMs (a second,
+// partial wave doubles the kernel time), each slice at least 4 k-tiles
 static int choose_splits(int tiles, int k_tiles) {
-  int s = (148 + tiles - 1) / tiles;
+  int s = 148 / std::max(1, tiles);
   s = std::max(1, std::min(s, k_tiles / 4));
   return s;
 }
@@ -193,7 +197,8 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     m->bn[i] = 64;
     Gs[i].adam = &m->st->adam;
   }
-  m->bn[G_E12] = 128;
+  // wide tiles where N is large or K is long: half the L2 operand re-reads
+  m->bn[G_E12] = m->bn[G_ROUTE_MEM] = m->bn[G_F] = m->bn[G_DZ2] = kWideBN;
   auto b = [&](int id) { return Builder{&Gs[id], m->bn[id]}; };
   Tensor4* w = M.w;
   // forward
@@ -298,8 +303,8 @@ static int allocate(fade_model* m) {
   memset(&M, 0, sizeof(M));
   M.d = d;
   M.sl = m->sl;
-  // split-K factors sized to ~one wave of 148 SMs (BN = 64 tiles)
-  const int tiles = cdiv(B, kBM) * cdiv(H, 64);
+  // split-K factors sized to ~one wave of 148 SMs (kWideBN tiles)
+  const int tiles = cdiv(B, kBM) * cdiv(H, kWideBN);
   M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
   M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
   M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));

@@ -154,19 +154,27 @@ static int launch_cfg(GemmParams& G, cudaStream_t st) {
 }
 
 int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
-  int t = 0, et = 1;
+  int t = 0, et = 0, out = 0;
   for (int q = 0; q < G.nprob; ++q) {
     G.prob[q].tile_begin = t;
     t += G.prob[q].tiles_m * G.prob[q].tiles_n * G.prob[q].splits;
     et = std::max(et, epi_tiles(G.prob[q].epi, BN));
+    out = std::max(out, epi_out_tiles(G.prob[q].epi, BN));
   }
   G.total_tiles = t;
   if (t == 0) return FADE_OK;
-  if (BN == 64 && et == 1) return launch_cfg<64, 1>(G, st);
+  auto fits = [&](int alias_tiles) {
+    if (et == 0 && out > alias_tiles) {
+      set_last_error("GEMM epilogue tiles exceed the pipeline smem they alias");
+      return false;
+    }
+    return true;
+  };
+  if (BN == 64 && et == 0 && fits(GemmCfg<64, 0>::kAliasTiles)) return launch_cfg<64, 0>(G, st);
   if (BN == 64 && et == 2) return launch_cfg<64, 2>(G, st);
   if (BN == 64 && et == 3) return launch_cfg<64, 3>(G, st);
-  if (BN == 128 && et == 2) return launch_cfg<128, 2>(G, st);
-  if (BN == 128 && et == 3) return launch_cfg<128, 3>(G, st);
+  if (BN == 128 && et == 0 && fits(GemmCfg<128, 0>::kAliasTiles)) return launch_cfg<128, 0>(G, st);
+  if (BN == 256 && et == 0 && fits(GemmCfg<256, 0>::kAliasTiles)) return launch_cfg<256, 0>(G, st);
   set_last_error("unsupported GEMM tile configuration");
   return FADE_ERR_USAGE;
 }

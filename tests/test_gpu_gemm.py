@@ -32,7 +32,7 @@ def run(M, N, K, a_trans, b_trans, splits=1, bn=128):
 
 
 @pytest.mark.parametrize("a_trans,b_trans", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("bn", [64, 128])
+@pytest.mark.parametrize("bn", [64, 128, 256])
 def test_majors(a_trans, b_trans, bn):
     assert run(256, 256, 512, a_trans, b_trans, bn=bn) < 3e-3
 
@@ -47,5 +47,7 @@ def test_shapes(shape):
 
 
 @pytest.mark.parametrize("splits", [2, 4, 8])
-def test_split_k(splits):
-    assert run(512, 512, 8192, 0, 0, splits=splits, bn=64) < 3e-3
+@pytest.mark.parametrize("bn", [64, 256])
+def test_split_k(splits, bn):
+    assert run(512, 512, 8192, 0, 0, splits=splits, bn=bn) < 3e-3
+    assert run(200, 300, 4000, 0, 1, splits=splits, bn=bn) < 3e-3   # ragged M: slices clip

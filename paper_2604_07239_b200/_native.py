@@ -61,7 +61,8 @@ SIGNATURES = {
     "fade_bench_compress_steps": (i32, [vp, vp, i64, i64, i64, P(vp), P(i32), vp]),
     "fade_model_stream": (i32, [vp, P(vp)]),
     "fade_bench_probe": (i32, [vp, i32, i32, P(f64), P(f64), P(f64)]),
-    "fade_debug_gemm": (i32, [vp, i64, i32, vp, i64, i32, vp, i64, i32, i32, i32, i32, i32, vp]),
+    "fade_debug_gemm": (i32, [vp, i64, i32, vp, i64, i32, vp, i64, i32, i32, i32, i32, i32, i32,
+                              vp]),
 }
 
 

@@ -164,14 +164,26 @@ static int choose_splits(int tiles, int k_tiles) {
 struct Builder {
   GemmParams* G;
   int BN;
-  int add(const GemmDesc& d) {
+  int add(GemmDesc d) {
     if (G->nprob >= kMaxProblems) {
       set_last_error("too many GEMM problems in one group");
       return FADE_ERR_USAGE;
     }
+    d.cluster_n = G->cluster_n;
     return gemm_setup(&G->prob[G->nprob++], d, BN);
   }
 };
+
+// N-cluster size for operand-A multicast: the largest of 4, 2 that divides the
+// N-tile count of every problem in the group
+static int cluster_for(int BN, std::initializer_list<int> ns) {
+  for (int c : {4, 2}) {
+    bool ok = true;
+    for (int n : ns) ok = ok && (cdiv(n, BN) % c == 0);
+    if (ok) return c;
+  }
+  return 1;
+}
 
 static GemmDesc gd(const float* A, long long lda, int at, const float* B, long long ldb, int bt,
                    int M, int N, int K, int epi, float* C, long long ldc) {
@@ -199,6 +211,22 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   }
   // wide tiles where N is large or K is long: half the L2 operand re-reads
   m->bn[G_E12] = m->bn[G_ROUTE_MEM] = m->bn[G_F] = m->bn[G_DZ2] = kWideBN;
+  // weight-gradient GEMMs and the GeGLU backward: wide tiles too, with their
+  // Adam p/m/v (a1/a2) inputs streamed through the idle stages
+  m->bn[G_DWIDE] = kWideBN;
+  // the big Adam GEMMs: 128-wide tiles at two CTAs per SM, so one CTA's
+  // streamed Adam epilogue overlaps the other's mainloop
+  for (int id : {G_W12, G_WF, G_WROUTE_WMEM}) {
+    m->bn[id] = 128;
+    Gs[id].occ = 2;
+  }
+  // Operand-A multicast over N-clusters is implemented and tested
+  // (tests/test_gpu_gemm.py::test_cluster_multicast) but measured slower at
+  // every FADE shape on B200 (the cluster lock-steps its stage releases), so
+  // the schedule runs unclustered.
+  constexpr bool kUseClusters = false;
+  for (int id : {G_ROUTE_MEM, G_E12, G_F, G_DZ2})
+    Gs[id].cluster_n = kUseClusters ? cluster_for(kWideBN, {H, 2 * Ep}) : 1;
   auto b = [&](int id) { return Builder{&Gs[id], m->bn[id]}; };
   Tensor4* w = M.w;
   // forward
@@ -244,7 +272,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     // tiles cover whole 64-column interleave blocks of dA12
     TRY(b(G_DWIDE).add(g));
     Gs[G_DWIDE].prob[0].N = Ep;
-    Gs[G_DWIDE].prob[0].tiles_n = cdiv(Ep, 64);
+    Gs[G_DWIDE].prob[0].tiles_n = cdiv(Ep, m->bn[G_DWIDE]);
   }
   {
     GemmDesc g = gd(a.da12, 2LL * Ep, 0, w[P_W_E1].p, 2LL * Ep, 1, B, H, 2 * Ep, EPI_STORE, a.ws_dz2, H);
@@ -308,7 +336,7 @@ static int allocate(fade_model* m) {
   M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
   M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
   M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
-  M.emb_chunk = 4;
+  M.emb_chunk = 2;
 
   struct Item { void** ptr; size_t bytes; };
   std::vector<Item> items;

@@ -89,7 +89,9 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   // B: b_trans == 0 -> B[k*ldb + n] (N-major); 1 -> B[n*ldb + k] (K-major)
   P->b_mn = d.b_trans ? 0 : 1;
   int s;
-  if (!P->a_mn) s = make_tmap_kmajor(&P->ta, d.A, d.M, d.K, d.lda, kBM);
+  // under an N-cluster each CTA loads kBM/cluster_n rows of a K-major A stage
+  const int cn = std::max(1, d.cluster_n);
+  if (!P->a_mn) s = make_tmap_kmajor(&P->ta, d.A, d.M, d.K, d.lda, kBM / cn);
   else s = make_tmap_mnmajor(&P->ta, d.A, d.M, d.K, d.lda);
   if (s) return s;
   if (!P->b_mn) s = make_tmap_kmajor(&P->tb, d.B, d.N, d.K, d.ldb, BN);
@@ -137,25 +139,30 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   return s;
 }
 
-template <int BN, int ET>
+template <int BN, int ET, int OCC = 1>
 static int launch_cfg(GemmParams& G, cudaStream_t st) {
-  using Cfg = GemmCfg<BN, ET>;
+  using Cfg = GemmCfg<BN, ET, OCC>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN, ET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN, ET, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     Cfg::kSmem);
   });
   FADE_CUDA_TRY(attr_err);
-  FADE_CUDA_TRY(launch_pdl(k_gemm_tf32<BN, ET>, dim3(G.total_tiles), dim3(kGemmThreads),
-                           (size_t)Cfg::kSmem, st, G));
+  FADE_CUDA_TRY(launch_pdl_cluster(k_gemm_tf32<BN, ET, OCC>, dim3(G.total_tiles), dim3(kGemmThreads),
+                                   (size_t)Cfg::kSmem, st, G.cluster_n, G));
   FADE_CUDA_TRY(cudaGetLastError());
   return FADE_OK;
 }
 
 int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   int t = 0, et = 0, out = 0;
+  if (G.cluster_n < 1) G.cluster_n = 1;
   for (int q = 0; q < G.nprob; ++q) {
+    if (G.prob[q].tiles_n % G.cluster_n) {   // a cluster must not straddle m-blocks
+      set_last_error("GEMM N-tiles not divisible by the cluster size");
+      return FADE_ERR_USAGE;
+    }
     G.prob[q].tile_begin = t;
     t += G.prob[q].tiles_m * G.prob[q].tiles_n * G.prob[q].splits;
     et = std::max(et, epi_tiles(G.prob[q].epi, BN));
@@ -170,6 +177,11 @@ int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
     }
     return true;
   };
+  if (G.occ == 2) {   // two CTAs per SM: one's epilogue overlaps the other's mainloop
+    if (BN == 128 && et == 0 && fits(GemmCfg<128, 0, 2>::kAliasTiles)) return launch_cfg<128, 0, 2>(G, st);
+    set_last_error("unsupported 2-CTA/SM GEMM configuration");
+    return FADE_ERR_USAGE;
+  }
   if (BN == 64 && et == 0 && fits(GemmCfg<64, 0>::kAliasTiles)) return launch_cfg<64, 0>(G, st);
   if (BN == 64 && et == 2) return launch_cfg<64, 2>(G, st);
   if (BN == 64 && et == 3) return launch_cfg<64, 3>(G, st);

@@ -9,7 +9,16 @@
 
 namespace fade {
 
-constexpr int kRowThreads = 128;
+constexpr int kRowMax = 512;
+constexpr int kBmmThreads = 128;
+
+// One CTA per stream row with one thread per row element (H = 512 -> 512
+// threads): B = 512 rows alone give only ~3.5 CTAs per SM, so the parallelism
+// has to come from inside the row to keep enough loads in flight.
+static int row_threads(int width) {
+  const int t = (width + 31) / 32 * 32;
+  return t < 128 ? 128 : (t > kRowMax ? kRowMax : t);
+}
 
 // LayerNorm statistics of a row held in shared memory (ops.py:94-101):
 // mu = mean(x); var = mean((x-mu)^2); inv = 1/sqrt(var + eps)
@@ -17,13 +26,13 @@ __device__ __forceinline__ void ln_stats(const float* xs, int n, float* red, flo
                                          float* inv_out) {
   float s = 0.f;
   for (int j = threadIdx.x; j < n; j += blockDim.x) s += xs[j];
-  const float mu = block_sum<kRowThreads / 32>(s, red) / (float)n;
+  const float mu = block_sum_rt(s, red) / (float)n;
   float q = 0.f;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const float c = xs[j] - mu;
     q += c * c;
   }
-  const float var = block_sum<kRowThreads / 32>(q, red) / (float)n;
+  const float var = block_sum_rt(q, red) / (float)n;
   *mu_out = mu;
   *inv_out = __fdiv_rn(1.0f, __fsqrt_rn(var + kLnEps));
 }
@@ -39,13 +48,13 @@ __device__ __forceinline__ void ln_bwd_means(const float* gs, const float* xhat_
     s1 += gg;
     s2 += gg * xhat_row[j];
   }
-  *m1 = block_sum<kRowThreads / 32>(s1, red) / (float)n;
-  *m2 = block_sum<kRowThreads / 32>(s2, red) / (float)n;
+  *m1 = block_sum_rt(s1, red) / (float)n;
+  *m2 = block_sum_rt(s2, red) / (float)n;
 }
 
 // ---------------------------------------------------------------------------
 // trunk + local stream forward (model.py:118-137)
-__global__ void __launch_bounds__(kRowThreads) k_trunk_fwd(ModelPtrs M, const uint8_t* src,
+__global__ void __launch_bounds__(kRowMax) k_trunk_fwd(ModelPtrs M, const uint8_t* src,
                                                            long long ld_src, int use_col) {
   pdl_enter();
   const Dims d = M.d;
@@ -108,17 +117,17 @@ __global__ void __launch_bounds__(kRowThreads) k_trunk_fwd(ModelPtrs M, const ui
     float* crow = M.a.cache + (long long)b * d.C;
     const int n4 = (d.C - d.D) / 4;      // float4 count to move
     constexpr int U = 4;
-    for (int base = 0; base < n4; base += U * kRowThreads) {
+    for (int base = 0; base < n4; base += U * (int)blockDim.x) {
       float4 r[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int q = base + u * kRowThreads + tid;
+        const int q = base + u * (int)blockDim.x + tid;
         if (q < n4) r[u] = *(const float4*)(crow + d.D + 4 * q);
       }
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int q = base + u * kRowThreads + tid;
+        const int q = base + u * (int)blockDim.x + tid;
         if (q < n4) *(float4*)(crow + 4 * q) = r[u];
       }
       __syncthreads();
@@ -178,12 +187,12 @@ void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (3 * d.H + (2 + d.K) * d.D * d.D + d.D + 2 * d.T + 32) +
                       sizeof(int) * d.T;
-  launch_pdl(k_trunk_fwd, dim3(d.B), dim3(kRowThreads), smem, s, M, src, ld_src, use_col);
+  launch_pdl(k_trunk_fwd, dim3(d.B), dim3(row_threads(M.d.H)), smem, s, M, src, ld_src, use_col);
 }
 
 // ---------------------------------------------------------------------------
 // global stream finish + router + mixer LayerNorm (model.py:128-153)
-__global__ void __launch_bounds__(kRowThreads) k_mix_fwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax) k_mix_fwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -212,14 +221,14 @@ __global__ void __launch_bounds__(kRowThreads) k_mix_fwd(ModelPtrs M) {
   __syncthreads();
   // router statistics for the metrics tape (model.py:197-199)
   {
-    const float s = block_sum<kRowThreads / 32>(asum, red);
+    const float s = block_sum_rt(asum, red);
     float mn = warp_max(-amin), mx = warp_max(amax);
-    __shared__ float rmn[4], rmx[4];
+    __shared__ float rmn[32], rmx[32];
     if ((tid & 31) == 0) { rmn[tid >> 5] = mn; rmx[tid >> 5] = mx; }
     __syncthreads();
     if (tid == 0) {
       float a = rmn[0], c = rmx[0];
-      for (int w = 1; w < kRowThreads / 32; ++w) { a = fmaxf(a, rmn[w]); c = fmaxf(c, rmx[w]); }
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { a = fmaxf(a, rmn[w]); c = fmaxf(c, rmx[w]); }
       M.a.alpha_row[3 * b + 0] = s;
       M.a.alpha_row[3 * b + 1] = -a;
       M.a.alpha_row[3 * b + 2] = c;
@@ -238,11 +247,11 @@ __global__ void __launch_bounds__(kRowThreads) k_mix_fwd(ModelPtrs M) {
 }
 
 void launch_mix_fwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_mix_fwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_mix_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // per-stream persistent memory: u[b] = zd[b] @ W_U[b]  (ops.py:44-54)
-__global__ void __launch_bounds__(kRowThreads) k_bmm_fwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kBmmThreads) k_bmm_fwd(ModelPtrs M) {
   pdl_enter();
   const int X = M.d.X, b = blockIdx.x;
   extern __shared__ float zs[];
@@ -257,11 +266,11 @@ __global__ void __launch_bounds__(kRowThreads) k_bmm_fwd(ModelPtrs M) {
 }
 
 void launch_bmm_fwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_bmm_fwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * M.d.X, s, M);
+  launch_pdl(k_bmm_fwd, dim3(M.d.B), dim3(kBmmThreads), sizeof(float) * M.d.X, s, M);
 }
 
 // self-gated coarse refiner + FNR LayerNorm (model.py:156-167)
-__global__ void __launch_bounds__(kRowThreads) k_coarse_fwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax) k_coarse_fwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -291,11 +300,11 @@ __global__ void __launch_bounds__(kRowThreads) k_coarse_fwd(ModelPtrs M) {
 }
 
 void launch_coarse_fwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_coarse_fwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_coarse_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // FNR output: split-K reduce, LayerNorm, gelu, residual (model.py:170-172)
-__global__ void __launch_bounds__(kRowThreads) k_out_fwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax) k_out_fwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -326,7 +335,7 @@ __global__ void __launch_bounds__(kRowThreads) k_out_fwd(ModelPtrs M) {
 }
 
 void launch_out_fwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_out_fwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_out_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // ---------------------------------------------------------------------------
@@ -479,7 +488,7 @@ __device__ __forceinline__ void adam_update(const AdamScalars& a, float g, float
 // backward row kernels
 
 // h = gelu(LN(npre)) + lam_out * h_c   (model.py:170-172 backward)
-__global__ void __launch_bounds__(kRowThreads) k_out_bwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax) k_out_bwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -500,7 +509,7 @@ __global__ void __launch_bounds__(kRowThreads) k_out_bwd(ModelPtrs M) {
     M.a.dhc[rH + j] = dh * lam;
   }
   __syncthreads();
-  const float ls = block_sum<kRowThreads / 32>(lsum, red);
+  const float ls = block_sum_rt(lsum, red);
   if (tid == 0) rr[M.sl.lam_out] = ls;
   float m1, m2;
   const float* g = M.w[P_OUT_LN_G].p;
@@ -511,11 +520,11 @@ __global__ void __launch_bounds__(kRowThreads) k_out_bwd(ModelPtrs M) {
 }
 
 void launch_out_bwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_out_bwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_out_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // z2 = LN(h_c); h_c = inner * sigmoid(cpre) + lam_mix * h_mix   (backward)
-__global__ void __launch_bounds__(kRowThreads) k_coarse_bwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax) k_coarse_bwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -546,17 +555,17 @@ __global__ void __launch_bounds__(kRowThreads) k_coarse_bwd(ModelPtrs M) {
     M.a.dcpre[rH + j] = dhc * M.a.inner[rH + j] * gt * (1.0f - gt);
     lsum += dhc * M.a.h_mix[rH + j];
   }
-  const float ls = block_sum<kRowThreads / 32>(lsum, red);
+  const float ls = block_sum_rt(lsum, red);
   if (tid == 0) rr[M.sl.lam_mix] = ls;
 }
 
 void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_coarse_bwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_coarse_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // per-stream memory backward + its Adam step in one streaming pass
 // (ops.py:48-52 for the gradients, optim.py:25-44 for the update)
-__global__ void __launch_bounds__(kRowThreads) k_bmm_bwd(ModelPtrs M, int grad_only) {
+__global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_only) {
   pdl_enter();
   const int X = M.d.X, b = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(kRowThreads) k_bmm_bwd(ModelPtrs M, int grad_o
   // one warp per row i; lanes cover 4 consecutive columns each (float4), so
   // the read-modify-write of p, m, v is one coalesced 512-byte pass per row
 #pragma unroll 2
-  for (int i = w; i < X; i += kRowThreads / 32) {
+  for (int i = w; i < X; i += kBmmThreads / 32) {
     float acc = 0.f;
     const float zi = zds[i];
     for (int j4 = lane; j4 < X4; j4 += 32) {
@@ -606,11 +615,11 @@ __global__ void __launch_bounds__(kRowThreads) k_bmm_bwd(ModelPtrs M, int grad_o
 }
 
 void launch_bmm_bwd(const ModelPtrs& M, int grad_only, cudaStream_t s) {
-  launch_pdl(k_bmm_bwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * 2 * M.d.X, s, M, grad_only);
+  launch_pdl(k_bmm_bwd, dim3(M.d.B), dim3(kBmmThreads), sizeof(float) * 2 * M.d.X, s, M, grad_only);
 }
 
 // mixer LayerNorm + router mix + global-stream gelu (model.py:128-153 backward)
-__global__ void __launch_bounds__(kRowThreads) k_mix_bwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax) k_mix_bwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -645,16 +654,16 @@ __global__ void __launch_bounds__(kRowThreads) k_mix_bwd(ModelPtrs M) {
     M.a.dx_part[rH + j] = dhg * lam_mem;
     lsum += dhg * M.a.x[rH + j];
   }
-  const float ls = block_sum<kRowThreads / 32>(lsum, red);
+  const float ls = block_sum_rt(lsum, red);
   if (tid == 0) rr[M.sl.lam_mem] = ls;
 }
 
 void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_mix_bwd, dim3(M.d.B), dim3(kRowThreads), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_mix_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
 // trunk + local stream backward (model.py:118-137 backward)
-__global__ void __launch_bounds__(kRowThreads) k_trunk_bwd(ModelPtrs M, const uint8_t* src,
+__global__ void __launch_bounds__(kRowMax) k_trunk_bwd(ModelPtrs M, const uint8_t* src,
                                                            long long ld_src, int use_col) {
   pdl_enter();
   const Dims d = M.d;
@@ -784,12 +793,12 @@ void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
                       cudaStream_t s) {
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (4 * d.H + d.K * d.D * d.D + 3 * d.D + 32);
-  launch_pdl(k_trunk_bwd, dim3(d.B), dim3(kRowThreads), smem, s, M, src, ld_src, use_col);
+  launch_pdl(k_trunk_bwd, dim3(d.B), dim3(row_threads(M.d.H)), smem, s, M, src, ld_src, use_col);
 }
 
 // Column sums of the per-row reduction buffer + dlogits (b_head), in a fixed
 // order, then Adam on the small-parameter arena.  Also the step loss.
-constexpr int kColWarps = 32;
+constexpr int kColWarps = 8;
 __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int grad_only,
                                                                double* losses) {
   pdl_enter();

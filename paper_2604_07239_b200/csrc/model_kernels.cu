@@ -37,6 +37,18 @@ __device__ __forceinline__ void ln_stats(const float* xs, int n, float* red, flo
   *inv_out = __fdiv_rn(1.0f, __fsqrt_rn(var + kLnEps));
 }
 
+// Fixed-order reduction of S split-K partial planes at element idx: four
+// independent accumulators (slices s = k mod 4) keep the loads in flight.
+__device__ __forceinline__ float split_sum(const float* __restrict__ ws, long long plane,
+                                           long long idx, int S) {
+  // (the unrolled-by-4 loop resolves a[s & 3] to registers; measured faster
+  // than a hand-split main/remainder loop)
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int s = 0; s < S; ++s) a[s & 3] += ws[s * plane + idx];
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
 // LayerNorm backward over one row (ops.py:103-113): returns dx into dxs (smem or
 // regs written by caller).  g = upstream grad (smem), xhat (global row), gain.
 __device__ __forceinline__ void ln_bwd_means(const float* gs, const float* xhat_row,
@@ -54,10 +66,15 @@ __device__ __forceinline__ void ln_bwd_means(const float* gs, const float* xhat_
 
 // ---------------------------------------------------------------------------
 // trunk + local stream forward (model.py:118-137)
-__global__ void __launch_bounds__(kRowMax) k_trunk_fwd(ModelPtrs M, const uint8_t* src,
-                                                           long long ld_src, int use_col) {
+// DT/TT/KT > 0: compile-time embed width, context length, conv taps (the
+// default geometry), so index math folds to shifts and the tap loops unroll;
+// 0 = runtime geometry
+template <int DT, int TT, int KT>
+__global__ void __launch_bounds__(kRowMax, 2) k_trunk_fwd(ModelPtrs M, const uint8_t* src,
+                                                       long long ld_src, int use_col) {
   pdl_enter();
-  const Dims d = M.d;
+  Dims d = M.d;
+  if (DT) { d.D = DT; d.T = TT; d.K = KT; d.H = DT * TT; }
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
   float* es = sm;                         // raw embedding row [H]
@@ -187,7 +204,10 @@ void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (3 * d.H + (2 + d.K) * d.D * d.D + d.D + 2 * d.T + 32) +
                       sizeof(int) * d.T;
-  launch_pdl(k_trunk_fwd, dim3(d.B), dim3(row_threads(M.d.H)), smem, s, M, src, ld_src, use_col);
+  if (d.D == 32 && d.T == 16 && d.K == 3)
+    launch_pdl(k_trunk_fwd<32, 16, 3>, dim3(d.B), dim3(row_threads(d.H)), smem, s, M, src, ld_src, use_col);
+  else
+    launch_pdl(k_trunk_fwd<0, 0, 0>, dim3(d.B), dim3(row_threads(d.H)), smem, s, M, src, ld_src, use_col);
 }
 
 // ---------------------------------------------------------------------------
@@ -205,7 +225,7 @@ __global__ void __launch_bounds__(kRowMax) k_mix_fwd(ModelPtrs M) {
   float asum = 0.f, amin = 3.4e38f, amax = -3.4e38f;
   for (int j = tid; j < d.H; j += blockDim.x) {
     float up = 0.f;
-    for (int s = 0; s < M.splits_mem; ++s) up += M.a.ws_mem[s * plane + rH + j];
+    up = split_sum(M.a.ws_mem, plane, rH + j, M.splits_mem);
     const float hg = gelu_f(up) + M.a.x[rH + j] * lam;
     const float al = sigmoid_f(M.a.rpre[rH + j]);
     const float hmx = al * hg + (1.0f - al) * M.a.h_l[rH + j];
@@ -315,7 +335,7 @@ __global__ void __launch_bounds__(kRowMax) k_out_fwd(ModelPtrs M) {
   const long long plane = (long long)d.B * d.H;
   for (int j = tid; j < d.H; j += blockDim.x) {
     float acc = 0.f;
-    for (int s = 0; s < M.splits_f; ++s) acc += M.a.ws_f[s * plane + rH + j];
+    acc = split_sum(M.a.ws_f, plane, rH + j, M.splits_f);
     np_[j] = acc;
   }
   __syncthreads();
@@ -536,7 +556,7 @@ __global__ void __launch_bounds__(kRowMax) k_coarse_bwd(ModelPtrs M) {
   float* rr = M.a.rowred + (long long)b * M.sl.rowred;
   for (int j = tid; j < d.H; j += blockDim.x) {
     float acc = 0.f;
-    for (int s = 0; s < M.splits_dz2; ++s) acc += M.a.ws_dz2[s * plane + rH + j];
+    acc = split_sum(M.a.ws_dz2, plane, rH + j, M.splits_dz2);
     dz[j] = acc;
     rr[M.sl.ref_g + j] = acc * M.a.z2_hat[rH + j];
     rr[M.sl.ref_b + j] = acc;
@@ -663,10 +683,12 @@ void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s) {
 }
 
 // trunk + local stream backward (model.py:118-137 backward)
-__global__ void __launch_bounds__(kRowMax) k_trunk_bwd(ModelPtrs M, const uint8_t* src,
-                                                           long long ld_src, int use_col) {
+template <int DT, int TT, int KT>
+__global__ void __launch_bounds__(kRowMax, 2) k_trunk_bwd(ModelPtrs M, const uint8_t* src,
+                                                       long long ld_src, int use_col) {
   pdl_enter();
-  const Dims d = M.d;
+  Dims d = M.d;
+  if (DT) { d.D = DT; d.T = TT; d.K = KT; d.H = DT * TT; }
   const int b = blockIdx.x, tid = threadIdx.x;
   extern __shared__ float sm[];
   float* dxs = sm;                        // [H] dx, later dxf
@@ -793,7 +815,10 @@ void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
                       cudaStream_t s) {
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (4 * d.H + d.K * d.D * d.D + 3 * d.D + 32);
-  launch_pdl(k_trunk_bwd, dim3(d.B), dim3(row_threads(M.d.H)), smem, s, M, src, ld_src, use_col);
+  if (d.D == 32 && d.T == 16 && d.K == 3)
+    launch_pdl(k_trunk_bwd<32, 16, 3>, dim3(d.B), dim3(row_threads(d.H)), smem, s, M, src, ld_src, use_col);
+  else
+    launch_pdl(k_trunk_bwd<0, 0, 0>, dim3(d.B), dim3(row_threads(d.H)), smem, s, M, src, ld_src, use_col);
 }
 
 // Column sums of the per-row reduction buffer + dlogits (b_head), in a fixed
@@ -807,11 +832,22 @@ __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int 
   const int c = blockIdx.x * 32 + lane;
   const int R = M.sl.rowred;
   const int total = R + kAlphabet;
-  float s = 0.f;
+  // 4 independent accumulators keep 4 loads in flight per thread; they are
+  // combined in a fixed order, so the sum is still deterministic
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   if (c < total) {
-    for (int b = w; b < M.d.B; b += kColWarps)
-      s += (c < R) ? M.a.rowred[(long long)b * R + c] : M.a.dlogits[(long long)b * kAlphabet + (c - R)];
+    const float* base = (c < R) ? M.a.rowred + c : M.a.dlogits + (c - R);
+    const long long ld = (c < R) ? R : kAlphabet;
+    int b = w;
+    for (; b + 3 * kColWarps < M.d.B; b += 4 * kColWarps) {
+      a0 += base[(long long)b * ld];
+      a1 += base[(long long)(b + kColWarps) * ld];
+      a2 += base[(long long)(b + 2 * kColWarps) * ld];
+      a3 += base[(long long)(b + 3 * kColWarps) * ld];
+    }
+    for (; b < M.d.B; b += kColWarps) a0 += base[(long long)b * ld];
   }
+  const float s = (a0 + a1) + (a2 + a3);
   part[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < total) {
@@ -863,13 +899,22 @@ __global__ void __launch_bounds__(256) k_emb_part(ModelPtrs M, const uint8_t* sr
   for (int q = threadIdx.x; q < kAlphabet * d.D; q += blockDim.x) out[q] = acc[q];
 }
 
-__global__ void k_emb_adam(ModelPtrs M, int nchunks, int grad_only) {
+// 32 embedding elements per CTA (lanes) x 8 warps over the chunk partials,
+// combined in a fixed order
+__global__ void __launch_bounds__(256) k_emb_adam(ModelPtrs M, int nchunks, int grad_only) {
   pdl_enter();
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ float part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q = blockIdx.x * 32 + lane;
   const int n = kAlphabet * M.d.D;
-  if (q >= n) return;
+  float s = 0.f;
+  if (q < n)
+    for (int c = w; c < nchunks; c += 8) s += M.a.emb_part[(long long)c * n + q];
+  part[w][lane] = s;
+  __syncthreads();
+  if (w != 0 || q >= n) return;
   float g = 0.f;
-  for (int c = 0; c < nchunks; ++c) g += M.a.emb_part[(long long)c * n + q];
+  for (int k = 0; k < 8; ++k) g += part[k][lane];
   Tensor4 t = M.w[P_EMB];
   if (grad_only) t.g[q] = g;
   else adam_update(M.st->adam, g, t.p + q, t.m + q, t.v + q);
@@ -879,7 +924,7 @@ void launch_emb_grad(const ModelPtrs& M, const uint8_t* src, long long ld_src, i
                      int grad_only, cudaStream_t s) {
   const int nchunks = cdiv(M.d.B, M.emb_chunk);
   launch_pdl(k_emb_part, dim3(nchunks), dim3(256), sizeof(float) * kAlphabet * M.d.D, s, M, src, ld_src, use_col);
-  launch_pdl(k_emb_adam, dim3(cdiv(kAlphabet * M.d.D, 256)), dim3(256), 0, s, M, nchunks, grad_only);
+  launch_pdl(k_emb_adam, dim3(cdiv(kAlphabet * M.d.D, 32)), dim3(256), 0, s, M, nchunks, grad_only);
 }
 
 __global__ void k_advance(StepState* st, int trained) {

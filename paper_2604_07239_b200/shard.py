@@ -1,0 +1,84 @@
+"""Multi-GPU compression: independent chunk shards, one process per GPU.
+
+SURVEY.md section 8e: the input is cut into G contiguous chunks; every rank
+compresses its chunk with its own model and B streams on its own device (no
+collective on the hot path).  The only exchange is host-side: rank 0 gathers
+each shard's stream table and bytes and writes one v2 container
+(`container.pack_shards`).  Decompression is equally independent: any rank can
+decode any shard.
+
+`torch.distributed` is plumbing here (object gather over gloo or NCCL); the
+compute is the per-rank `run_pipelined_compress` on the rank's device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import replace
+
+from .config import ModelConfig
+
+
+def shard_bounds(n: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous [lo, hi) byte ranges, sizes differing by at most one."""
+    base, extra = divmod(n, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def compress_shard(data: bytes, cfg: ModelConfig, rank: int, world: int, compress_fn=None):
+    """Compress this rank's chunk; returns its CompressResult."""
+    from .pipeline import run_pipelined_compress
+    lo, hi = shard_bounds(len(data), world)[rank]
+    fn = compress_fn or run_pipelined_compress
+    return fn(data[lo:hi], cfg)
+
+
+def compress_sharded(data: bytes, cfg: ModelConfig, group=None, compress_fn=None) -> bytes | None:
+    """Collective entry point: every rank calls it with the same `data`.
+
+    Returns the v2 container on rank 0 and None elsewhere.  Each rank's device
+    must already be selected (`torch.cuda.set_device(local_rank)`).
+    """
+    import torch.distributed as dist
+
+    from . import container
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    res = compress_shard(data, cfg, rank, world, compress_fn)
+    # host-side gather of (stream table, bytes) -- the only exchange step
+    payload = (res.partition.original_length, res.cfg, [bytes(s) for s in res.streams], res.losses)
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object(payload, gathered, dst=0, group=group)
+    if rank != 0:
+        return None
+    from .pipeline import CompressResult, StreamPartition
+    results = []
+    for orig, rcfg, streams, losses in gathered:
+        rcfg = rcfg or replace(cfg, batch=max(1, len(streams)))
+        results.append(CompressResult(streams, rcfg, StreamPartition.from_length(orig, len(streams)),
+                                      losses))
+    return container.pack_shards(results, cfg)
+
+
+def decompress_sharded(blob: bytes, group=None) -> bytes | None:
+    """Each rank decodes its share of the shards; rank 0 returns the bytes."""
+    import torch.distributed as dist
+
+    from . import container
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    shards = container.unpack_shards(blob)
+    mine = {i: container.decompress_shard(s, fp) for i, (s, fp) in enumerate(shards)
+            if i % world == rank}
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object(mine, gathered, dst=0, group=group)
+    if rank != 0:
+        return None
+    parts = {}
+    for g in gathered:
+        parts.update(g)
+    return b"".join(parts[i] for i in range(len(shards)))

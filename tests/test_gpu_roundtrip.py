@@ -116,3 +116,16 @@ def test_bits_per_byte_default_1mib_within_half_percent():
     rel = (ours - ref) / ref
     print(f"default 1 MiB: ours {ours} B vs reference {ref} B ({100 * rel:+.3f}%)")
     assert abs(rel) < 0.005, (ours, ref)
+
+
+def test_sharded_v2_container_round_trip():
+    """independent shards (here run one after another on one GPU),
+    host-side gather into a v2 container, decode back bit-exactly."""
+    from paper_2604_07239_b200 import container, corpus
+    from paper_2604_07239_b200.pipeline import run_pipelined_compress
+    from paper_2604_07239_b200.shard import shard_bounds
+    data = corpus.make_modal(9000, 2, chunk=3000)
+    cfg = tiny()
+    res = [run_pipelined_compress(data[lo:hi], cfg) for lo, hi in shard_bounds(len(data), 3)]
+    blob = container.pack_shards(res, cfg)
+    assert container.decompress_bytes(blob) == data

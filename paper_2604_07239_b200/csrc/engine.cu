@@ -303,15 +303,20 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     }
     return g;
   };
-  TRY(b(G_WHEAD).add(adam(gd(a.h, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD])));
-  TRY(b(G_WF).add(adam(gd(a.wide, Ep, 1, a.dnpre, H, 0, E, H, B, EPI_ADAM, nullptr, H), w[P_W_F])));
+  // W_head rides in the W_f launch and W_down in the W_up/W_cgate launch:
+  // fewer side-stream kernels (each costs a fixed ~10 us of latency)
+  {
+    auto bl = b(G_WF);
+    TRY(bl.add(adam(gd(a.h, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD])));
+    TRY(bl.add(adam(gd(a.wide, Ep, 1, a.dnpre, H, 0, E, H, B, EPI_ADAM, nullptr, H), w[P_W_F])));
+  }
   TRY(b(G_W12).add(adam(gd(a.z2, H, 1, a.da12, 2LL * Ep, 0, H, 2 * Ep, B, EPI_ADAM, nullptr, 2LL * Ep), w[P_W_E1])));
   {
     auto bl = b(G_WUP_WCGATE);
     TRY(bl.add(adam(gd(a.u, X, 1, a.dinner, H, 0, X, H, B, EPI_ADAM, nullptr, H), w[P_W_UP])));
     TRY(bl.add(adam(gd(a.h_mix, H, 1, a.dcpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_CGATE])));
+    TRY(bl.add(adam(gd(a.z, H, 1, a.dzd, X, 0, H, X, B, EPI_ADAM, nullptr, X), w[P_W_DOWN])));
   }
-  TRY(b(G_WDOWN).add(adam(gd(a.z, H, 1, a.dzd, X, 0, H, X, B, EPI_ADAM, nullptr, X), w[P_W_DOWN])));
   {
     auto bl = b(G_WROUTE_WMEM);
     TRY(bl.add(adam(gd(a.x, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE])));
@@ -337,6 +342,10 @@ static int allocate(fade_model* m) {
   M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
   M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
   M.emb_chunk = 2;
+  M.lr = m->cfg.lr;
+  M.beta1 = m->cfg.beta1;
+  M.beta2 = m->cfg.beta2;
+  M.adam_eps = m->cfg.adam_eps;
 
   struct Item { void** ptr; size_t bytes; };
   std::vector<Item> items;
@@ -442,35 +451,34 @@ static int fork_side(fade_model* m, int k) {
   return FADE_OK;
 }
 
-static int backward(fade_model* m, const StepIO& io, bool grad_only, double* losses) {
+// advance = 1: the step counts as trained (the last kernel moves the column
+// and the step count; Predictor.train_step semantics, model.py:214)
+static int backward(fade_model* m, const StepIO& io, bool grad_only, double* losses, int advance) {
   cudaStream_t s = m->s_main, side = m->s_side;
   const ModelPtrs& M = m->M;
-  if (!grad_only) launch_adam_prep(M, m->cfg.lr, m->cfg.beta1, m->cfg.beta2, m->cfg.adam_eps, s);
+  // the Adam step counter and bias-correction scalars were prepared by the
+  // head kernel (HeadArgs.adam_prep); the last kernel advances the column
   TRY(run_gemm(m, G_DH, s));
-  TRY(fork_side(m, 0));
-  TRY(run_gemm(m, G_WHEAD, side, grad_only));
   launch_out_bwd(M, s);
   TRY(run_gemm(m, G_DWIDE, s));
   TRY(fork_side(m, 1));
-  TRY(run_gemm(m, G_WF, side, grad_only));
+  TRY(run_gemm(m, G_WF, side, grad_only));          // + W_head
   TRY(run_gemm(m, G_DZ2, s));
   TRY(fork_side(m, 2));
   TRY(run_gemm(m, G_W12, side, grad_only));
   launch_coarse_bwd(M, s);
   TRY(run_gemm(m, G_DU_DHMC, s));
-  TRY(fork_side(m, 3));
-  TRY(run_gemm(m, G_WUP_WCGATE, side, grad_only));
   launch_bmm_bwd(M, grad_only, s);
   TRY(run_gemm(m, G_DZ, s));
   TRY(fork_side(m, 4));
-  TRY(run_gemm(m, G_WDOWN, side, grad_only));
+  TRY(run_gemm(m, G_WUP_WCGATE, side, grad_only));  // + W_down
   launch_mix_bwd(M, s);
   TRY(run_gemm(m, G_DXR_DBLOCK, s));
   TRY(fork_side(m, 5));
   TRY(run_gemm(m, G_WROUTE_WMEM, side, grad_only));
   launch_trunk_bwd(M, io.src, io.ld_src, io.use_col, s);
   launch_small_adam(M, grad_only, losses, s);
-  launch_emb_grad(M, io.src, io.ld_src, io.use_col, grad_only, s);
+  launch_emb_grad(M, io.src, io.ld_src, io.use_col, grad_only, advance, s);
   CK(cudaEventRecord(m->ev_side_done, side));
   CK(cudaStreamWaitEvent(s, m->ev_side_done, 0));
   CK(cudaGetLastError());
@@ -719,9 +727,9 @@ int fade_model_train_step(fade_model_t* m, const uint8_t* targets, double* loss,
   io.head.xent = 1;
   io.head.tgt = m->tgt_buf;
   io.head.ld_tgt = 1;
+  io.head.adam_prep = 1;
   launch_head(m->M, io.head, m->s_main);     // dlogits + nll for these targets
-  TRY(backward(m, io, false, m->loss_buf));
-  launch_advance(m->M, 1, m->s_main);
+  TRY(backward(m, io, false, m->loss_buf, 1));
   CK(cudaStreamSynchronize(m->s_main));
   TRY(check_error(m, err));
   CK(cudaMemcpy(loss, m->loss_buf, sizeof(double), cudaMemcpyDeviceToHost));
@@ -779,7 +787,7 @@ int fade_model_loss_grads(fade_model_t* m, const uint8_t* ctx, const uint8_t* ta
   io.head.tgt = m->tgt_buf;
   io.head.ld_tgt = 1;
   TRY(forward(m, io, true));
-  TRY(backward(m, io, true, m->loss_buf));
+  TRY(backward(m, io, true, m->loss_buf, 0));
   CK(cudaMemcpyAsync(m->M.a.cache, m->cache_snap, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
   CK(cudaStreamSynchronize(m->s_main));
   TRY(check_error(m, nullptr));
@@ -864,6 +872,7 @@ static int compress_step(fade_model_t* m, fade_coder_t* c, const uint8_t* data, 
   io.head.tgt = data;
   io.head.ld_tgt = L;
   io.head.tgt_use_col = 1;
+  io.head.adam_prep = 1;
   TRY(forward(m, io, true));
   if (pipelined) {
     // CSPP: the coder stream drains this step's table while the model
@@ -875,9 +884,8 @@ static int compress_step(fade_model_t* m, fade_coder_t* c, const uint8_t* data, 
   } else {
     launch_encode_col(c->e, m->d.B, data, L, m->M.a.cum, m->s_main);
   }
-  TRY(backward(m, io, false, losses));
+  TRY(backward(m, io, false, losses, 1));
   if (pipelined) CK(cudaStreamWaitEvent(m->s_main, m->ev_enc[0], 0));
-  launch_advance(m->M, 1, m->s_main);
   CK(cudaGetLastError());
   return FADE_OK;
 }
@@ -1018,13 +1026,13 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
     io.head.dpos = ds.pos;
     io.head.dcode = ds.code;
     io.head.drng = ds.rng;
+    io.head.adam_prep = 1;
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
     // decode(i) -> train(i) -> predict(i+1) is strictly serial (pipeline.py:364-376)
     status = forward(m, io, true);
-    if (status == FADE_OK) status = backward(m, io, false, dloss);
-    launch_advance(m->M, 1, m->s_main);
+    if (status == FADE_OK) status = backward(m, io, false, dloss, 1);
     cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
     if (status != FADE_OK) return status;
     CK(ce);

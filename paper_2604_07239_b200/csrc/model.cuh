@@ -81,6 +81,7 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   StepState* st;
   int splits_mem, splits_f, splits_dz2;
   int emb_chunk;       // streams per embedding-gradient partial
+  double lr, beta1, beta2, adam_eps;   // Adam hyperparameters (config.py:29-32)
 };
 
 // row kernels (model_kernels.cu)
@@ -93,6 +94,7 @@ void launch_out_fwd(const ModelPtrs& M, cudaStream_t s);
 // head: fp64 softmax -> quantiser -> cum slot; optional probs; optional
 // cross-entropy with targets read from tgt (+ col) or decoded in place.
 struct HeadArgs {
+  int adam_prep;            // 1: this step trains -> t += 1 and Adam scalars (optim.py:26-30)
   int want_probs;
   int xent;                 // 1: emit dlogits + nll
   const uint8_t* tgt;       // target bytes (row b at tgt + b*ld_tgt + col) or null
@@ -110,8 +112,6 @@ struct HeadArgs {
   unsigned long long* drng;
 };
 void launch_head(const ModelPtrs& M, const HeadArgs& h, cudaStream_t s);
-void launch_adam_prep(const ModelPtrs& M, double lr, double b1, double b2, double eps,
-                      cudaStream_t s);
 void launch_out_bwd(const ModelPtrs& M, cudaStream_t s);
 void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s);
 void launch_bmm_bwd(const ModelPtrs& M, int grad_only, cudaStream_t s);
@@ -119,8 +119,8 @@ void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s);
 void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s);
 void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, cudaStream_t s);
+// advance = 1 also moves the step state to the next column (last kernel of a step)
 void launch_emb_grad(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
-                     int grad_only, cudaStream_t s);
-void launch_advance(const ModelPtrs& M, int trained, cudaStream_t s);
+                     int grad_only, int advance, cudaStream_t s);
 
 }  // namespace fade

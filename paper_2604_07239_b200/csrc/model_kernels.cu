@@ -383,6 +383,8 @@ __device__ __forceinline__ double block_sum_d256(double v, double* red) {
   return t;
 }
 
+__device__ void adam_prep_dev(StepState* st, double lr, double b1, double b2, double eps);
+
 __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
   pdl_enter();
   __shared__ QuantSmem qs;
@@ -399,6 +401,8 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
   __syncthreads();
   if (!isfinite(lg)) atomicOr(&bad_s, 1);
   __syncthreads();
+  if (H.adam_prep && b == 0 && i == 0)
+    adam_prep_dev(st, M.lr, M.beta1, M.beta2, M.adam_eps);
   if (bad_s) {
     if (i == 0) record_error(st, col, b, 3);
     return;
@@ -470,9 +474,9 @@ void launch_head(const ModelPtrs& M, const HeadArgs& h, cudaStream_t s) {
   launch_pdl(k_head, dim3(M.d.B), dim3(256), 0, s, M, h);
 }
 
-// Adam bias-correction scalars from the device step counter (optim.py:26-30)
-__global__ void k_adam_prep(StepState* st, double lr, double b1, double b2, double eps) {
-  pdl_enter();
+// Adam bias-correction scalars from the device step counter (optim.py:26-30);
+// run by one thread of the head kernel of every training step
+__device__ void adam_prep_dev(StepState* st, double lr, double b1, double b2, double eps) {
   const long long t = ++st->adam_t;
   const double c1 = 1.0 - pow(b1, (double)t);
   const double c2 = 1.0 - pow(b2, (double)t);
@@ -487,10 +491,6 @@ __global__ void k_adam_prep(StepState* st, double lr, double b1, double b2, doub
   st->adam = a;
 }
 
-void launch_adam_prep(const ModelPtrs& M, double lr, double b1, double b2, double eps,
-                      cudaStream_t s) {
-  launch_pdl(k_adam_prep, dim3(1), dim3(1), 0, s, M.st, lr, b1, b2, eps);
-}
 
 __device__ __forceinline__ void adam_update(const AdamScalars& a, float g, float* p, float* m,
                                             float* v) {
@@ -901,8 +901,15 @@ __global__ void __launch_bounds__(256) k_emb_part(ModelPtrs M, const uint8_t* sr
 
 // 32 embedding elements per CTA (lanes) x 8 warps over the chunk partials,
 // combined in a fixed order
-__global__ void __launch_bounds__(256) k_emb_adam(ModelPtrs M, int nchunks, int grad_only) {
+__global__ void __launch_bounds__(256) k_emb_adam(ModelPtrs M, int nchunks, int grad_only,
+                                                  int advance) {
   pdl_enter();
+  // last kernel of a trained step: move to the next column (nothing in this
+  // kernel reads it; the next step waits for our completion)
+  if (advance && blockIdx.x == 0 && threadIdx.x == 0) {
+    M.st->col += 1;
+    M.st->step_count += 1;
+  }
   __shared__ float part[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int q = blockIdx.x * 32 + lane;
@@ -921,20 +928,12 @@ __global__ void __launch_bounds__(256) k_emb_adam(ModelPtrs M, int nchunks, int 
 }
 
 void launch_emb_grad(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
-                     int grad_only, cudaStream_t s) {
+                     int grad_only, int advance, cudaStream_t s) {
   const int nchunks = cdiv(M.d.B, M.emb_chunk);
   launch_pdl(k_emb_part, dim3(nchunks), dim3(256), sizeof(float) * kAlphabet * M.d.D, s, M, src, ld_src, use_col);
-  launch_pdl(k_emb_adam, dim3(cdiv(kAlphabet * M.d.D, 32)), dim3(256), 0, s, M, nchunks, grad_only);
+  launch_pdl(k_emb_adam, dim3(cdiv(kAlphabet * M.d.D, 32)), dim3(256), 0, s, M, nchunks, grad_only,
+             advance);
 }
 
-__global__ void k_advance(StepState* st, int trained) {
-  pdl_enter();
-  st->col += 1;
-  st->step_count += trained;
-}
-
-void launch_advance(const ModelPtrs& M, int trained, cudaStream_t s) {
-  launch_pdl(k_advance, dim3(1), dim3(1), 0, s, M.st, trained);
-}
 
 }  // namespace fade

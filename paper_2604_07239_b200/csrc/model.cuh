@@ -114,7 +114,7 @@ struct HeadArgs {
 void launch_head(const ModelPtrs& M, const HeadArgs& h, cudaStream_t s);
 void launch_out_bwd(const ModelPtrs& M, cudaStream_t s);
 void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s);
-void launch_bmm_bwd(const ModelPtrs& M, int grad_only, cudaStream_t s);
+void launch_bmm_bwd(const ModelPtrs& M, int grad_only, int mode, cudaStream_t s);
 void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s);
 void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s);

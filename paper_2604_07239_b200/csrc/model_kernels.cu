@@ -585,7 +585,10 @@ void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s) {
 
 // per-stream memory backward + its Adam step in one streaming pass
 // (ops.py:48-52 for the gradients, optim.py:25-44 for the update)
-__global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_only) {
+// mode bit 0: input gradient dzd (reads W_U once -- the model stream's part);
+// mode bit 1: W_U gradient + Adam (the 24 B/param RMW -- run on the side
+// stream after the input gradient has read the old W_U)
+__global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_only, int mode) {
   pdl_enter();
   const int X = M.d.X, b = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -606,6 +609,7 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
   const int X4 = X / 4;      // X is a multiple of 4 (ModelConfig.device_check)
   // one warp per row i; lanes cover 4 consecutive columns each (float4), so
   // the read-modify-write of p, m, v is one coalesced 512-byte pass per row
+  const bool do_dx = mode & 1, do_upd = mode & 2;
 #pragma unroll 2
   for (int i = w; i < X; i += kBmmThreads / 32) {
     float acc = 0.f;
@@ -616,7 +620,8 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
       const float4 du4 = *(const float4*)(dus + 4 * j4);
       acc += du4.x * p.x + du4.y * p.y + du4.z * p.z + du4.w * p.w;
       const float4 g = make_float4(zi * du4.x, zi * du4.y, zi * du4.z, zi * du4.w);
-      if (grad_only) {
+      if (!do_upd) {
+      } else if (grad_only) {
         Wg[q] = g;
       } else {
         float4 m = Wm[q], v = Wv[q];
@@ -629,13 +634,16 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
         Wv[q] = v;
       }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) M.a.dzd[(long long)b * X + i] = acc;
+    if (do_dx) {
+      acc = warp_sum(acc);
+      if (lane == 0) M.a.dzd[(long long)b * X + i] = acc;
+    }
   }
 }
 
-void launch_bmm_bwd(const ModelPtrs& M, int grad_only, cudaStream_t s) {
-  launch_pdl(k_bmm_bwd, dim3(M.d.B), dim3(kBmmThreads), sizeof(float) * 2 * M.d.X, s, M, grad_only);
+void launch_bmm_bwd(const ModelPtrs& M, int grad_only, int mode, cudaStream_t s) {
+  launch_pdl(k_bmm_bwd, dim3(M.d.B), dim3(kBmmThreads), sizeof(float) * 2 * M.d.X, s, M, grad_only,
+             mode);
 }
 
 // mixer LayerNorm + router mix + global-stream gelu (model.py:128-153 backward)

@@ -326,6 +326,9 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
 }
 
 static int run_gemm(fade_model* m, int id, cudaStream_t s, bool grad_only = false) {
+  static const int dbg_skip = getenv("FADE_DBG_SKIP") ? atoi(getenv("FADE_DBG_SKIP")) : 0;
+  if ((dbg_skip & 1) && s == m->s_side) return FADE_OK;
+  if ((dbg_skip & 2) && s != m->s_side) return FADE_OK;
   return gemm_launch(grad_only ? m->Gg[id] : m->G[id], m->bn[id], s);
 }
 
@@ -555,9 +558,15 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   d.K = cfg->conv_kernel;
   m->sl = make_small_layout(d);
   CK(cudaSetDevice(device));
-  CK(cudaStreamCreateWithFlags(&m->s_main, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&m->s_side, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&m->s_coder, cudaStreamNonBlocking));
+  // the model stream is the critical path: its CTAs take SM slots ahead of
+  // the side stream's (HBM-bound) weight-update GEMMs when both are pending
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  static const int dbg_prio = getenv("FADE_DBG_PRIO") ? atoi(getenv("FADE_DBG_PRIO")) : 1;
+  if (!dbg_prio) prio_hi = prio_lo;
+  CK(cudaStreamCreateWithPriority(&m->s_main, cudaStreamNonBlocking, prio_hi));
+  CK(cudaStreamCreateWithPriority(&m->s_side, cudaStreamNonBlocking, prio_lo));
+  CK(cudaStreamCreateWithPriority(&m->s_coder, cudaStreamNonBlocking, prio_hi));
   for (auto& e : m->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
     CK(cudaEventCreateWithFlags(&m->ev_cum[i], cudaEventDisableTiming));

@@ -11,6 +11,11 @@ namespace fade {
 
 constexpr int kRowMax = 512;
 constexpr int kBmmThreads = 128;
+constexpr int kBmmRows = 32;      // W_U rows per k_bmm_bwd CTA
+// The trunk kernels run 256 threads x 2 elements at <= 64 registers so four
+// CTAs fit per SM: all B = 512 rows are resident in ONE wave (512-thread CTAs
+// at 64 registers fit two per SM -> two serial waves of a latency-bound row).
+constexpr int kTrunkThreads = 256;
 
 // One CTA per stream row with one thread per row element (H = 512 -> 512
 // threads): B = 512 rows alone give only ~3.5 CTAs per SM, so the parallelism
@@ -70,7 +75,7 @@ __device__ __forceinline__ void ln_bwd_means(const float* gs, const float* xhat_
 // default geometry), so index math folds to shifts and the tap loops unroll;
 // 0 = runtime geometry
 template <int DT, int TT, int KT>
-__global__ void __launch_bounds__(kRowMax, 2) k_trunk_fwd(ModelPtrs M, const uint8_t* src,
+__global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, const uint8_t* src,
                                                        long long ld_src, int use_col) {
   pdl_enter();
   Dims d = M.d;
@@ -205,14 +210,14 @@ void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
   const size_t smem = sizeof(float) * (3 * d.H + (2 + d.K) * d.D * d.D + d.D + 2 * d.T + 32) +
                       sizeof(int) * d.T;
   if (d.D == 32 && d.T == 16 && d.K == 3)
-    launch_pdl(k_trunk_fwd<32, 16, 3>, dim3(d.B), dim3(row_threads(d.H)), smem, s, M, src, ld_src, use_col);
+    launch_pdl(k_trunk_fwd<32, 16, 3>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
   else
-    launch_pdl(k_trunk_fwd<0, 0, 0>, dim3(d.B), dim3(row_threads(d.H)), smem, s, M, src, ld_src, use_col);
+    launch_pdl(k_trunk_fwd<0, 0, 0>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
 }
 
 // ---------------------------------------------------------------------------
 // global stream finish + router + mixer LayerNorm (model.py:128-153)
-__global__ void __launch_bounds__(kRowMax) k_mix_fwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -290,7 +295,7 @@ void launch_bmm_fwd(const ModelPtrs& M, cudaStream_t s) {
 }
 
 // self-gated coarse refiner + FNR LayerNorm (model.py:156-167)
-__global__ void __launch_bounds__(kRowMax) k_coarse_fwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax, 4) k_coarse_fwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -324,7 +329,7 @@ void launch_coarse_fwd(const ModelPtrs& M, cudaStream_t s) {
 }
 
 // FNR output: split-K reduce, LayerNorm, gelu, residual (model.py:170-172)
-__global__ void __launch_bounds__(kRowMax) k_out_fwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax, 4) k_out_fwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -508,7 +513,7 @@ __device__ __forceinline__ void adam_update(const AdamScalars& a, float g, float
 // backward row kernels
 
 // h = gelu(LN(npre)) + lam_out * h_c   (model.py:170-172 backward)
-__global__ void __launch_bounds__(kRowMax) k_out_bwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax, 4) k_out_bwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -544,7 +549,7 @@ void launch_out_bwd(const ModelPtrs& M, cudaStream_t s) {
 }
 
 // z2 = LN(h_c); h_c = inner * sigmoid(cpre) + lam_mix * h_mix   (backward)
-__global__ void __launch_bounds__(kRowMax) k_coarse_bwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax, 4) k_coarse_bwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -595,10 +600,9 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
   extern __shared__ float sm[];
   float* dus = sm;          // [X]
   float* zds = sm + X;      // [X]
-  for (int i = threadIdx.x; i < X; i += blockDim.x) {
-    dus[i] = M.a.du[(long long)b * X + i];
-    zds[i] = M.a.zd[(long long)b * X + i];
-  }
+  for (int i = threadIdx.x; i < X; i += blockDim.x) dus[i] = M.a.du[(long long)b * X + i];
+  const int i0 = blockIdx.y * kBmmRows, i1 = min(X, i0 + kBmmRows);
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) zds[i - i0] = M.a.zd[(long long)b * X + i];
   __syncthreads();
   const long long base = (long long)b * X * X;
   float4* __restrict__ Wp = (float4*)(M.w[P_W_MIX].p + base);
@@ -608,12 +612,14 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
   const AdamScalars a = M.st->adam;
   const int X4 = X / 4;      // X is a multiple of 4 (ModelConfig.device_check)
   // one warp per row i; lanes cover 4 consecutive columns each (float4), so
-  // the read-modify-write of p, m, v is one coalesced 512-byte pass per row
+  // the read-modify-write of p, m, v is one coalesced 512-byte pass per row.
+  // A CTA owns kBmmRows rows of one stream: 4x more CTAs than streams keeps
+  // the HBM-bound RMW evenly spread over the 148 SMs.
   const bool do_dx = mode & 1, do_upd = mode & 2;
-#pragma unroll 2
-  for (int i = w; i < X; i += kBmmThreads / 32) {
+#pragma unroll 4
+  for (int i = i0 + w; i < i1; i += kBmmThreads / 32) {
     float acc = 0.f;
-    const float zi = zds[i];
+    const float zi = zds[i - i0];
     for (int j4 = lane; j4 < X4; j4 += 32) {
       const long long q = (long long)i * X4 + j4;
       float4 p = Wp[q];
@@ -642,12 +648,12 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
 }
 
 void launch_bmm_bwd(const ModelPtrs& M, int grad_only, int mode, cudaStream_t s) {
-  launch_pdl(k_bmm_bwd, dim3(M.d.B), dim3(kBmmThreads), sizeof(float) * 2 * M.d.X, s, M, grad_only,
-             mode);
+  launch_pdl(k_bmm_bwd, dim3(M.d.B, cdiv(M.d.X, kBmmRows)), dim3(kBmmThreads),
+             sizeof(float) * (M.d.X + kBmmRows), s, M, grad_only, mode);
 }
 
 // mixer LayerNorm + router mix + global-stream gelu (model.py:128-153 backward)
-__global__ void __launch_bounds__(kRowMax) k_mix_bwd(ModelPtrs M) {
+__global__ void __launch_bounds__(kRowMax, 4) k_mix_bwd(ModelPtrs M) {
   pdl_enter();
   const Dims d = M.d;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -692,7 +698,7 @@ void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s) {
 
 // trunk + local stream backward (model.py:118-137 backward)
 template <int DT, int TT, int KT>
-__global__ void __launch_bounds__(kRowMax, 2) k_trunk_bwd(ModelPtrs M, const uint8_t* src,
+__global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, const uint8_t* src,
                                                        long long ld_src, int use_col) {
   pdl_enter();
   Dims d = M.d;
@@ -824,14 +830,19 @@ void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (4 * d.H + d.K * d.D * d.D + 3 * d.D + 32);
   if (d.D == 32 && d.T == 16 && d.K == 3)
-    launch_pdl(k_trunk_bwd<32, 16, 3>, dim3(d.B), dim3(row_threads(d.H)), smem, s, M, src, ld_src, use_col);
+    launch_pdl(k_trunk_bwd<32, 16, 3>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
   else
-    launch_pdl(k_trunk_bwd<0, 0, 0>, dim3(d.B), dim3(row_threads(d.H)), smem, s, M, src, ld_src, use_col);
+    launch_pdl(k_trunk_bwd<0, 0, 0>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
 }
 
 // Column sums of the per-row reduction buffer + dlogits (b_head), in a fixed
 // order, then Adam on the small-parameter arena.  Also the step loss.
-constexpr int kColWarps = 8;
+constexpr int kColWarps = 16;
+constexpr int kColAcc = 8;
+// one CTA per 32 columns of the rowred/dlogits matrices; 16 warps x 8
+// independent accumulators keep 8 row loads in flight per thread (the column
+// sum is latency bound: 19.6 MB that just landed in L2).  Partials combine in
+// a fixed order, so the result is deterministic.
 __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int grad_only,
                                                                double* losses) {
   pdl_enter();
@@ -840,37 +851,39 @@ __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int 
   const int c = blockIdx.x * 32 + lane;
   const int R = M.sl.rowred;
   const int total = R + kAlphabet;
-  // 4 independent accumulators keep 4 loads in flight per thread; they are
-  // combined in a fixed order, so the sum is still deterministic
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  float acc[kColAcc];
+#pragma unroll
+  for (int k = 0; k < kColAcc; ++k) acc[k] = 0.f;
   if (c < total) {
     const float* base = (c < R) ? M.a.rowred + c : M.a.dlogits + (c - R);
     const long long ld = (c < R) ? R : kAlphabet;
     int b = w;
-    for (; b + 3 * kColWarps < M.d.B; b += 4 * kColWarps) {
-      a0 += base[(long long)b * ld];
-      a1 += base[(long long)(b + kColWarps) * ld];
-      a2 += base[(long long)(b + 2 * kColWarps) * ld];
-      a3 += base[(long long)(b + 3 * kColWarps) * ld];
+    for (; b + (kColAcc - 1) * kColWarps < M.d.B; b += kColAcc * kColWarps) {
+#pragma unroll
+      for (int k = 0; k < kColAcc; ++k) acc[k] += base[(long long)(b + k * kColWarps) * ld];
     }
-    for (; b < M.d.B; b += kColWarps) a0 += base[(long long)b * ld];
+    for (; b < M.d.B; b += kColWarps) acc[0] += base[(long long)b * ld];
   }
-  const float s = (a0 + a1) + (a2 + a3);
+  const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   part[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < total) {
     float g = 0.f;
+#pragma unroll
     for (int k = 0; k < kColWarps; ++k) g += part[k][lane];
     if (grad_only) M.small_g[c] = g;
     else adam_update(M.st->adam, g, M.small_p + c, M.small_m + c, M.small_v + c);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 32) {
+  if (blockIdx.x == 0 && w == 1) {
+    // mean cross-entropy: lane-strided partials, then a fixed xor tree
     double l = 0.0;
-    for (int b = 0; b < M.d.B; ++b) l += M.a.nll[b];
-    l /= (double)M.d.B;
-    StepState* st = M.st;
-    if (!isfinite(l)) record_error(st, st->col, 0, 5);
-    if (losses) losses[st->col - st->loss_base] = l;
+    for (int b = lane; b < M.d.B; b += 32) l += M.a.nll[b];
+    l = warp_sum_d(l) / (double)M.d.B;
+    if (lane == 0) {
+      StepState* st = M.st;
+      if (!isfinite(l)) record_error(st, st->col, 0, 5);
+      if (losses) losses[st->col - st->loss_base] = l;
+    }
   }
 }
 

@@ -329,6 +329,8 @@ static int run_gemm(fade_model* m, int id, cudaStream_t s, bool grad_only = fals
   static const int dbg_skip = getenv("FADE_DBG_SKIP") ? atoi(getenv("FADE_DBG_SKIP")) : 0;
   if ((dbg_skip & 1) && s == m->s_side) return FADE_OK;
   if ((dbg_skip & 2) && s != m->s_side) return FADE_OK;
+  static const long dbg_ids = getenv("FADE_DBG_SKIPID") ? atol(getenv("FADE_DBG_SKIPID")) : 0;
+  if (dbg_ids & (1L << id)) return FADE_OK;
   return gemm_launch(grad_only ? m->Gg[id] : m->G[id], m->bn[id], s);
 }
 

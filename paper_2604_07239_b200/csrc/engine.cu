@@ -169,21 +169,10 @@ struct Builder {
       set_last_error("too many GEMM problems in one group");
       return FADE_ERR_USAGE;
     }
-    d.cluster_n = G->cluster_n;
+    d.pair = G->pair;
     return gemm_setup(&G->prob[G->nprob++], d, BN);
   }
 };
-
-// N-cluster size for operand-A multicast: the largest of 4, 2 that divides the
-// N-tile count of every problem in the group
-static int cluster_for(int BN, std::initializer_list<int> ns) {
-  for (int c : {4, 2}) {
-    bool ok = true;
-    for (int n : ns) ok = ok && (cdiv(n, BN) % c == 0);
-    if (ok) return c;
-  }
-  return 1;
-}
 
 static GemmDesc gd(const float* A, long long lda, int at, const float* B, long long ldb, int bt,
                    int M, int N, int K, int epi, float* C, long long ldc) {
@@ -220,13 +209,16 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     m->bn[id] = 128;
     Gs[id].occ = 2;
   }
-  // Operand-A multicast over N-clusters is implemented and tested
-  // (tests/test_gpu_gemm.py::test_cluster_multicast) but measured slower at
-  // every FADE shape on B200 (the cluster lock-steps its stage releases), so
-  // the schedule runs unclustered.
-  constexpr bool kUseClusters = false;
-  for (int id : {G_ROUTE_MEM, G_E12, G_F, G_DZ2})
-    Gs[id].cluster_n = kUseClusters ? cluster_for(kWideBN, {H, 2 * Ep}) : 1;
+  // CTA pairs (cta_group::2, 256-row tiles): half the operand bytes per SM
+  // (W12 update and the GeGLU backward; measured slower for the narrower
+  // W_f / W_route / W_mem updates and the forward GEMMs)
+  static const long pair_ids = getenv("FADE_PAIR") ? atol(getenv("FADE_PAIR"))
+                                                   : (1L << G_W12) | (1L << G_DWIDE);
+  for (int id = 0; id < G_COUNT; ++id) {
+    if (!((pair_ids >> id) & 1) || m->bn[id] < 128) continue;
+    Gs[id].pair = 2;
+    if (Gs[id].occ == 2) m->bn[id] = 256;   // pair tiles 256 x 256 at two CTAs per SM
+  }
   auto b = [&](int id) { return Builder{&Gs[id], m->bn[id]}; };
   Tensor4* w = M.w;
   // forward

@@ -89,19 +89,19 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   // B: b_trans == 0 -> B[k*ldb + n] (N-major); 1 -> B[n*ldb + k] (K-major)
   P->b_mn = d.b_trans ? 0 : 1;
   int s;
-  // under an N-cluster each CTA loads kBM/cluster_n rows of a K-major A stage
-  const int cn = std::max(1, d.cluster_n);
-  if (!P->a_mn) s = make_tmap_kmajor(&P->ta, d.A, d.M, d.K, d.lda, kBM / cn);
+  // a CTA pair splits the B tile: each CTA stages BN/2 columns
+  const int pair = d.pair == 2 ? 2 : 1;
+  if (!P->a_mn) s = make_tmap_kmajor(&P->ta, d.A, d.M, d.K, d.lda, kBM);
   else s = make_tmap_mnmajor(&P->ta, d.A, d.M, d.K, d.lda);
   if (s) return s;
-  if (!P->b_mn) s = make_tmap_kmajor(&P->tb, d.B, d.N, d.K, d.ldb, BN);
+  if (!P->b_mn) s = make_tmap_kmajor(&P->tb, d.B, d.N, d.K, d.ldb, BN / pair);
   else s = make_tmap_mnmajor(&P->tb, d.B, d.N, d.K, d.ldb);
   if (s) return s;
   const int kt = cdiv(d.K, kBK);
   const int splits = std::max(1, std::min(d.splits, kt));
   P->k_tiles_per_split = cdiv(kt, splits);
   P->splits = cdiv(kt, P->k_tiles_per_split);   // no empty split
-  P->tiles_m = cdiv(d.M, kBM);
+  P->tiles_m = cdiv(d.M, kBM * pair);
   P->tiles_n = cdiv(d.N, BN);
   P->epi = d.epi;
   P->bias = d.bias;
@@ -139,30 +139,26 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   return s;
 }
 
-template <int BN, int ET, int OCC = 1>
+template <int BN, int ET, int OCC = 1, int PAIR = 1>
 static int launch_cfg(GemmParams& G, cudaStream_t st) {
-  using Cfg = GemmCfg<BN, ET, OCC>;
+  using Cfg = GemmCfg<BN, ET, OCC, PAIR>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN, ET, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg::kSmem);
+    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN, ET, OCC, PAIR>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
   });
   FADE_CUDA_TRY(attr_err);
-  FADE_CUDA_TRY(launch_pdl_cluster(k_gemm_tf32<BN, ET, OCC>, dim3(G.total_tiles), dim3(kGemmThreads),
-                                   (size_t)Cfg::kSmem, st, G.cluster_n, G));
+  FADE_CUDA_TRY(launch_pdl_cluster(k_gemm_tf32<BN, ET, OCC, PAIR>, dim3(G.total_tiles * PAIR),
+                                   dim3(kGemmThreads), (size_t)Cfg::kSmem, st, PAIR, G));
   FADE_CUDA_TRY(cudaGetLastError());
   return FADE_OK;
 }
 
 int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   int t = 0, et = 0, out = 0;
-  if (G.cluster_n < 1) G.cluster_n = 1;
+  if (G.pair != 2) G.pair = 1;
   for (int q = 0; q < G.nprob; ++q) {
-    if (G.prob[q].tiles_n % G.cluster_n) {   // a cluster must not straddle m-blocks
-      set_last_error("GEMM N-tiles not divisible by the cluster size");
-      return FADE_ERR_USAGE;
-    }
     G.prob[q].tile_begin = t;
     t += G.prob[q].tiles_m * G.prob[q].tiles_n * G.prob[q].splits;
     et = std::max(et, epi_tiles(G.prob[q].epi, BN));
@@ -177,6 +173,20 @@ int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
     }
     return true;
   };
+  if (G.pair == 2) {   // CTA pairs: 256-row tiles, B staged half per CTA
+    if (et != 0) {
+      set_last_error("CTA-pair GEMMs need a streamed (stage-aliased) epilogue");
+      return FADE_ERR_USAGE;
+    }
+    // two pairs per SM pair when the epilogue's output tiles fit the smaller
+    // stage ring (the streamed Adam epilogue does), else one
+    if (BN == 256 && G.occ == 2 && out <= GemmCfg<256, 0, 2, 2>::kAliasTiles)
+      return launch_cfg<256, 0, 2, 2>(G, st);
+    if (BN == 256 && fits(GemmCfg<256, 0, 1, 2>::kAliasTiles)) return launch_cfg<256, 0, 1, 2>(G, st);
+    if (BN == 128 && fits(GemmCfg<128, 0, 1, 2>::kAliasTiles)) return launch_cfg<128, 0, 1, 2>(G, st);
+    set_last_error("unsupported CTA-pair GEMM configuration");
+    return FADE_ERR_USAGE;
+  }
   if (G.occ == 2) {   // two CTAs per SM: one's epilogue overlaps the other's mainloop
     if (BN == 128 && et == 0 && fits(GemmCfg<128, 0, 2>::kAliasTiles)) return launch_cfg<128, 0, 2>(G, st);
     set_last_error("unsupported 2-CTA/SM GEMM configuration");

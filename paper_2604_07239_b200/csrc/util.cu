@@ -29,12 +29,12 @@ int fade_device_count(void) {
 //   `splits` partial slices at C + s*M*ldc.
 int fade_debug_gemm(const float* A, long long lda, int a_trans, const float* B, long long ldb,
                     int b_trans, float* C, long long ldc, int M, int N, int K, int splits, int bn,
-                    int cluster_n, void* stream) {
+                    int pair, void* stream) {
   GemmParams G;
   memset(&G, 0, sizeof(G));
-  G.cluster_n = cluster_n;
+  G.pair = pair;
   GemmDesc d{};
-  d.cluster_n = cluster_n;
+  d.pair = pair;
   d.A = A; d.lda = lda; d.a_trans = a_trans;
   d.B = B; d.ldb = ldb; d.b_trans = b_trans;
   d.M = M; d.N = N; d.K = K;

@@ -1,5 +1,5 @@
 """tcgen05 TF32 GEMM vs a plain torch fp64 reference: all operand majors, tile
-widths, split-K with ragged M, and N-clusters multicasting operand A."""
+widths, split-K with ragged M, and CTA pairs (cta_group::2, 256-row tiles)."""
 
 import pytest
 
@@ -8,7 +8,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def run(M, N, K, a_trans, b_trans, splits=1, bn=128, cluster=1):
+def run(M, N, K, a_trans, b_trans, splits=1, bn=128, pair=1):
     from paper_2604_07239_b200 import _native
     lib = _native.lib()
     g = torch.Generator(device="cuda").manual_seed(M * 131 + N * 7 + K)
@@ -19,7 +19,7 @@ def run(M, N, K, a_trans, b_trans, splits=1, bn=128, cluster=1):
     ldc = (N + 3) // 4 * 4
     C = torch.full((splits, M, ldc), float("nan"), device="cuda")
     st = lib.fade_debug_gemm(As.data_ptr(), As.shape[1], a_trans, Bs.data_ptr(), Bs.shape[1],
-                             b_trans, C.data_ptr(), ldc, M, N, K, splits, bn, cluster, None)
+                             b_trans, C.data_ptr(), ldc, M, N, K, splits, bn, pair, None)
     assert st == 0, _native.last_error()
     torch.cuda.synchronize()
     ref = (A.double() @ B.double())
@@ -52,9 +52,10 @@ def test_split_k(splits, bn):
     assert run(200, 300, 4000, 0, 1, splits=splits, bn=bn) < 3e-3   # ragged M: slices clip
 
 
-@pytest.mark.parametrize("cluster", [2, 4])
+@pytest.mark.parametrize("bn", [128, 256])
 @pytest.mark.parametrize("a_trans,b_trans", [(0, 0), (0, 1), (1, 0), (1, 1)])
-def test_cluster_multicast(cluster, a_trans, b_trans):
-    assert run(512, 1024, 512, a_trans, b_trans, bn=64, cluster=cluster) < 3e-3
-    assert run(300, 2048, 700, a_trans, b_trans, bn=256, cluster=cluster) < 3e-3
-    assert run(512, 512, 8192, a_trans, b_trans, splits=4, bn=128, cluster=cluster) < 3e-3
+def test_cta_pair(bn, a_trans, b_trans):
+    assert run(512, 1024, 512, a_trans, b_trans, bn=bn, pair=2) < 3e-3
+    assert run(300, 2048, 700, a_trans, b_trans, bn=bn, pair=2) < 3e-3     # ragged M and K
+    assert run(128, 512, 256, a_trans, b_trans, bn=bn, pair=2) < 3e-3      # empty second CTA rows
+    assert run(512, 512, 8192, a_trans, b_trans, splits=4, bn=bn, pair=2) < 3e-3

@@ -338,7 +338,6 @@ static int allocate(fade_model* m) {
   M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
   M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
   M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
-  M.emb_chunk = 2;
   M.lr = m->cfg.lr;
   M.beta1 = m->cfg.beta1;
   M.beta2 = m->cfg.beta2;
@@ -375,9 +374,9 @@ static int allocate(fade_model* m) {
   F(&a.da12, B * 2 * Ep); F(&a.ws_dz2, (long long)M.splits_dz2 * B * H); F(&a.dinner, B * H);
   F(&a.dcpre, B * H); F(&a.du, B * X); F(&a.dhm_c, B * H); F(&a.dzd, B * X); F(&a.dz, B * H);
   F(&a.drpre, B * H); F(&a.dupre, B * H); F(&a.dh_l, B * H); F(&a.dx_part, B * H);
-  F(&a.dx_r, B * H); F(&a.dblock, B * d.D); F(&a.demb, B * H);
+  F(&a.dx_r, B * H); F(&a.dblock, B * d.D);
   F(&a.rowred, B * m->sl.rowred);
-  F(&a.emb_part, (long long)cdiv(B, M.emb_chunk) * 256 * d.D);
+  items.push_back({(void**)&a.emb_acc, sizeof(long long) * 256 * (size_t)d.D});
   items.push_back({(void**)&m->st, sizeof(StepState)});
   items.push_back({(void**)&m->ctx_buf, (size_t)B * d.T});
   items.push_back({(void**)&m->tgt_buf, (size_t)B});
@@ -476,8 +475,7 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   TRY(fork_side(m, 5));
   TRY(run_gemm(m, G_WROUTE_WMEM, side, grad_only));
   launch_trunk_bwd(M, io.src, io.ld_src, io.use_col, s);
-  launch_small_adam(M, grad_only, losses, s);
-  launch_emb_grad(M, io.src, io.ld_src, io.use_col, grad_only, advance, s);
+  launch_small_adam(M, grad_only, losses, advance, s);
   CK(cudaEventRecord(m->ev_side_done, side));
   CK(cudaStreamWaitEvent(s, m->ev_side_done, 0));
   CK(cudaGetLastError());

@@ -67,9 +67,9 @@ struct Acts {        // saved activations and gradient scratch, all [B][ld]
   float *alpha_row;             // [B][3] per-row router stats (sum, min, max)
   // backward
   float *dlogits, *dh, *dhc, *dnpre, *da12, *ws_dz2, *dinner, *dcpre, *du, *dhm_c;
-  float *dzd, *dz, *drpre, *dupre, *dh_l, *dx_part, *dx_r, *dblock, *demb;
+  float *dzd, *dz, *drpre, *dupre, *dh_l, *dx_part, *dx_r, *dblock;
   float *rowred;                // [B][rowred]
-  float *emb_part;              // [chunks][256][D]
+  long long* emb_acc;           // [256][D] embedding gradient, fixed point (emb_to_fixed)
 };
 
 struct ModelPtrs {   // everything a row kernel may need, passed by value
@@ -80,7 +80,6 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   Acts a;
   StepState* st;
   int splits_mem, splits_f, splits_dz2;
-  int emb_chunk;       // streams per embedding-gradient partial
   double lr, beta1, beta2, adam_eps;   // Adam hyperparameters (config.py:29-32)
 };
 
@@ -118,9 +117,20 @@ void launch_bmm_bwd(const ModelPtrs& M, int grad_only, int mode, cudaStream_t s)
 void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s);
 void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s);
-void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, cudaStream_t s);
-// advance = 1 also moves the step state to the next column (last kernel of a step)
-void launch_emb_grad(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
-                     int grad_only, int advance, cudaStream_t s);
+// small-parameter + embedding Adam and the step loss; advance = 1 also moves
+// the step state to the next column (the last kernel of a trained step)
+void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, int advance,
+                       cudaStream_t s);
+
+// Embedding-gradient accumulator: 2^-48 fixed point in int64.  Integer
+// addition is associative, so atomics give a bit-reproducible sum (encoder
+// and decoder replay the same trajectory); 2^-48 resolution is far below the
+// fp32 rounding of the gradient values and |sum| < 2^15 leaves ample range.
+__device__ __forceinline__ long long emb_to_fixed(float g) {
+  return __double2ll_rn((double)g * 0x1p48);
+}
+__device__ __forceinline__ float emb_from_fixed(long long v) {
+  return (float)((double)v * 0x1p-48);
+}
 
 }  // namespace fade

@@ -714,9 +714,12 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   float* dv = dg + d.D;                   // [D] dvpre
   float* xt = dv + d.D;                   // [D]
   float* red = xt + d.D;                  // [32]
+  int* ctx = (int*)(red + 32);            // [T] context symbols
   const long long rH = (long long)b * d.H;
   float* rr = M.a.rowred + (long long)b * M.sl.rowred;
   const float* Wg = M.w[P_W_GATE].p;
+  const long long c0 = use_col ? M.st->col - d.T : 0;
+  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
   const float* Wv = M.w[P_W_VAL].p;
   // taps transposed to [tap][co][ci] so the input-gradient loop below reads
   // consecutive ci across lanes (no 32-way bank conflict)
@@ -821,14 +824,17 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     const float lh = M.a.loc_hat[rH + j];
     const float de = (dls[j] * lg[e] - locs[2 * t] - lh * locs[2 * t + 1]) *
                      M.a.loc_inv[(long long)b * d.T + t];
-    M.a.demb[rH + j] = de + dxs[j];
+    // embedding gradient (ops.py:234-243 scatter-add): integer adds commute,
+    // so the fixed-point sum is the same whatever order the rows arrive in
+    atomicAdd((unsigned long long*)&M.a.emb_acc[ctx[t] * d.D + e],
+              (unsigned long long)emb_to_fixed(de + dxs[j]));
   }
 }
 
 void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s) {
   const Dims& d = M.d;
-  const size_t smem = sizeof(float) * (4 * d.H + d.K * d.D * d.D + 3 * d.D + 32);
+  const size_t smem = sizeof(float) * (4 * d.H + d.K * d.D * d.D + 3 * d.D + 32) + sizeof(int) * d.T;
   if (d.D == 32 && d.T == 16 && d.K == 3)
     launch_pdl(k_trunk_bwd<32, 16, 3>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
   else
@@ -843,9 +849,24 @@ constexpr int kColAcc = 8;
 // independent accumulators keep 8 row loads in flight per thread (the column
 // sum is latency bound: 19.6 MB that just landed in L2).  Partials combine in
 // a fixed order, so the result is deterministic.
+// Extra CTAs past the column blocks apply the embedding update from the
+// fixed-point accumulator (and clear it for the next step).  Last kernel of a
+// step: with `advance` it moves the step state to the next column.
 __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int grad_only,
-                                                               double* losses) {
+                                                               double* losses, int col_blocks,
+                                                               int advance) {
   pdl_enter();
+  if ((int)blockIdx.x >= col_blocks) {
+    const int q = ((int)blockIdx.x - col_blocks) * blockDim.x + threadIdx.x;
+    if (q >= kAlphabet * M.d.D) return;
+    long long* acc = M.a.emb_acc + q;
+    const float g = emb_from_fixed(*acc);
+    *acc = 0;
+    Tensor4 t = M.w[P_EMB];
+    if (grad_only) t.g[q] = g;
+    else adam_update(M.st->adam, g, t.p + q, t.m + q, t.v + q);
+    return;
+  }
   __shared__ float part[kColWarps][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -883,78 +904,21 @@ __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int 
       StepState* st = M.st;
       if (!isfinite(l)) record_error(st, st->col, 0, 5);
       if (losses) losses[st->col - st->loss_base] = l;
-    }
-  }
-}
-
-void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, cudaStream_t s) {
-  const int total = M.sl.rowred + kAlphabet;
-  launch_pdl(k_small_adam, dim3(cdiv(total, 32)), dim3(32 * kColWarps), 0, s, M, grad_only, losses);
-}
-
-// embedding gradient: deterministic two-level scatter-add (ops.py:234-243)
-__global__ void __launch_bounds__(256) k_emb_part(ModelPtrs M, const uint8_t* src,
-                                                  long long ld_src, int use_col) {
-  pdl_enter();
-  const Dims d = M.d;
-  extern __shared__ float acc[];          // [256][D]
-  const int chunk = blockIdx.x;
-  for (int q = threadIdx.x; q < kAlphabet * d.D; q += blockDim.x) acc[q] = 0.f;
-  __syncthreads();
-  const int groups = blockDim.x / d.D;
-  const int g = threadIdx.x / d.D, e = threadIdx.x % d.D;
-  const long long c0 = use_col ? M.st->col - d.T : 0;
-  const int b0 = chunk * M.emb_chunk, b1 = min(d.B, b0 + M.emb_chunk);
-  if (g < groups) {
-    for (int b = b0; b < b1; ++b) {
-      const uint8_t* row = src + (long long)b * ld_src + c0;
-      for (int t = 0; t < d.T; ++t) {
-        const int sym = row[t];
-        if (sym % groups != g) continue;
-        acc[sym * d.D + e] += M.a.demb[(long long)b * d.H + t * d.D + e];
+      // nothing else in this grid reads the column; the next step waits for us
+      if (advance) {
+        st->col += 1;
+        st->step_count += 1;
       }
     }
   }
-  __syncthreads();
-  float* out = M.a.emb_part + (long long)chunk * kAlphabet * d.D;
-  for (int q = threadIdx.x; q < kAlphabet * d.D; q += blockDim.x) out[q] = acc[q];
 }
 
-// 32 embedding elements per CTA (lanes) x 8 warps over the chunk partials,
-// combined in a fixed order
-__global__ void __launch_bounds__(256) k_emb_adam(ModelPtrs M, int nchunks, int grad_only,
-                                                  int advance) {
-  pdl_enter();
-  // last kernel of a trained step: move to the next column (nothing in this
-  // kernel reads it; the next step waits for our completion)
-  if (advance && blockIdx.x == 0 && threadIdx.x == 0) {
-    M.st->col += 1;
-    M.st->step_count += 1;
-  }
-  __shared__ float part[8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int q = blockIdx.x * 32 + lane;
-  const int n = kAlphabet * M.d.D;
-  float s = 0.f;
-  if (q < n)
-    for (int c = w; c < nchunks; c += 8) s += M.a.emb_part[(long long)c * n + q];
-  part[w][lane] = s;
-  __syncthreads();
-  if (w != 0 || q >= n) return;
-  float g = 0.f;
-  for (int k = 0; k < 8; ++k) g += part[k][lane];
-  Tensor4 t = M.w[P_EMB];
-  if (grad_only) t.g[q] = g;
-  else adam_update(M.st->adam, g, t.p + q, t.m + q, t.v + q);
+void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, int advance,
+                       cudaStream_t s) {
+  const int col_blocks = cdiv(M.sl.rowred + kAlphabet, 32);
+  const int emb_blocks = cdiv(kAlphabet * M.d.D, 32 * kColWarps);
+  launch_pdl(k_small_adam, dim3(col_blocks + emb_blocks), dim3(32 * kColWarps), 0, s, M, grad_only,
+             losses, col_blocks, advance);
 }
-
-void launch_emb_grad(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
-                     int grad_only, int advance, cudaStream_t s) {
-  const int nchunks = cdiv(M.d.B, M.emb_chunk);
-  launch_pdl(k_emb_part, dim3(nchunks), dim3(256), sizeof(float) * kAlphabet * M.d.D, s, M, src, ld_src, use_col);
-  launch_pdl(k_emb_adam, dim3(cdiv(kAlphabet * M.d.D, 32)), dim3(256), 0, s, M, nchunks, grad_only,
-             advance);
-}
-
 
 }  // namespace fade

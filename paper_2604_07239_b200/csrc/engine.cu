@@ -161,6 +161,39 @@ static int choose_splits(int tiles, int k_tiles) {
   return s;
 }
 
+// Split-K factors of one launch group of narrow (64-wide tile) GEMMs:
+// repeatedly double the split of the problem with the most k-tiles per CTA
+// while the group stays within one wave of 148 CTAs and every slice keeps at
+// least 2 k-tiles.
+struct SplitPlan {
+  int id;
+  long long M, N, K;
+};
+static void plan_splits(ModelPtrs& M, std::initializer_list<SplitPlan> group) {
+  std::vector<SplitPlan> g(group);
+  std::vector<int> S(g.size(), 1);
+
+  auto tiles = [](const SplitPlan& p) { return (int)(cdiv(p.M, kBM) * cdiv(p.N, 64)); };
+  int total = 0;
+  for (auto& p : g) total += tiles(p);
+  for (;;) {
+    int best = -1;
+    int best_kt = 0;
+    for (size_t i = 0; i < g.size(); ++i) {
+      const int kt = (int)cdiv(g[i].K, kBK);
+      if (kt / (2 * S[i]) < 2 || total + tiles(g[i]) * S[i] > 148) continue;
+      if (kt / S[i] > best_kt) {
+        best_kt = kt / S[i];
+        best = (int)i;
+      }
+    }
+    if (best < 0) break;
+    total += tiles(g[best]) * S[best];
+    S[best] *= 2;
+  }
+  for (size_t i = 0; i < g.size(); ++i) M.sk[g[i].id].S = S[i];
+}
+
 struct Builder {
   GemmParams* G;
   int BN;
@@ -229,11 +262,18 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     g.splits = M.splits_mem;
     TRY(bl.add(g));
   }
-  TRY(b(G_DOWN).add(gd(a.z, H, 0, w[P_W_DOWN].p, X, 0, B, X, H, EPI_STORE, a.zd, X)));
+  // narrow GEMMs write split-K slices their consumer reduces (plan_splits)
+  auto sk = [&](GemmDesc g, int id) {
+    g.C = M.sk[id].ws;
+    g.ldc = g.N;
+    g.splits = M.sk[id].S;
+    return g;
+  };
+  TRY(b(G_DOWN).add(sk(gd(a.z, H, 0, w[P_W_DOWN].p, X, 0, B, X, H, EPI_STORE, nullptr, 0), S_ZD)));
   {
     auto bl = b(G_UP_CGATE);
-    TRY(bl.add(gd(a.u, X, 0, w[P_W_UP].p, H, 0, B, H, X, EPI_STORE, a.inner, H)));
-    TRY(bl.add(gd(a.h_mix, H, 0, w[P_W_CGATE].p, H, 0, B, H, H, EPI_STORE, a.cpre, H)));
+    TRY(bl.add(sk(gd(a.u, X, 0, w[P_W_UP].p, H, 0, B, H, X, EPI_STORE, nullptr, 0), S_INNER)));
+    TRY(bl.add(sk(gd(a.h_mix, H, 0, w[P_W_CGATE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_CPRE)));
   }
   {
     GemmDesc g = gd(a.z2, H, 0, w[P_W_E1].p, 2LL * Ep, 0, B, 2 * Ep, H, EPI_GEGLU, a.a12, 2LL * Ep);
@@ -248,12 +288,12 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     TRY(b(G_F).add(g));
   }
   {
-    GemmDesc g = gd(a.h, H, 0, w[P_W_HEAD].p, 256, 0, B, 256, H, EPI_STORE, a.logits, 256);
+    GemmDesc g = sk(gd(a.h, H, 0, w[P_W_HEAD].p, 256, 0, B, 256, H, EPI_STORE, nullptr, 0), S_LOGITS);
     g.bias = w[P_B_HEAD].p;
     TRY(b(G_HEAD).add(g));
   }
   // input gradients
-  TRY(b(G_DH).add(gd(a.dlogits, 256, 0, w[P_W_HEAD].p, 256, 1, B, H, 256, EPI_STORE, a.dh, H)));
+  TRY(b(G_DH).add(sk(gd(a.dlogits, 256, 0, w[P_W_HEAD].p, 256, 1, B, H, 256, EPI_STORE, nullptr, 0), S_DH)));
   {
     GemmDesc g = gd(a.dnpre, H, 0, w[P_W_F].p, H, 1, B, E, H, EPI_GEGLU_BWD, a.da12, 2LL * Ep);
     g.aux1 = a.a12;
@@ -273,15 +313,15 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   }
   {
     auto bl = b(G_DU_DHMC);
-    TRY(bl.add(gd(a.dinner, H, 0, w[P_W_UP].p, H, 1, B, X, H, EPI_STORE, a.du, X)));
-    TRY(bl.add(gd(a.dcpre, H, 0, w[P_W_CGATE].p, H, 1, B, H, H, EPI_STORE, a.dhm_c, H)));
+    TRY(bl.add(sk(gd(a.dinner, H, 0, w[P_W_UP].p, H, 1, B, X, H, EPI_STORE, nullptr, 0), S_DU)));
+    TRY(bl.add(sk(gd(a.dcpre, H, 0, w[P_W_CGATE].p, H, 1, B, H, H, EPI_STORE, nullptr, 0), S_DHMC)));
   }
-  TRY(b(G_DZ).add(gd(a.dzd, X, 0, w[P_W_DOWN].p, X, 1, B, H, X, EPI_STORE, a.dz, H)));
+  TRY(b(G_DZ).add(sk(gd(a.dzd, X, 0, w[P_W_DOWN].p, X, 1, B, H, X, EPI_STORE, nullptr, 0), S_DZ)));
   {
     auto bl = b(G_DXR_DBLOCK);
-    TRY(bl.add(gd(a.drpre, H, 0, w[P_W_ROUTE].p, H, 1, B, H, H, EPI_STORE, a.dx_r, H)));
-    TRY(bl.add(gd(a.dupre, H, 0, w[P_W_MEM].p + (long long)(C - d.D) * H, H, 1, B, d.D, H,
-                  EPI_STORE, a.dblock, d.D)));
+    TRY(bl.add(sk(gd(a.drpre, H, 0, w[P_W_ROUTE].p, H, 1, B, H, H, EPI_STORE, nullptr, 0), S_DXR)));
+    TRY(bl.add(sk(gd(a.dupre, H, 0, w[P_W_MEM].p + (long long)(C - d.D) * H, H, 1, B, d.D, H,
+                     EPI_STORE, nullptr, 0), S_DBLOCK)));
   }
   // weight gradients with the Adam step fused into the epilogue
   auto adam = [&](GemmDesc g, const Tensor4& t) {
@@ -338,6 +378,13 @@ static int allocate(fade_model* m) {
   M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
   M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
   M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
+  // Only the forward's narrow GEMMs split: in the backward the side stream's
+  // weight updates hold most SMs, and a 128-CTA input-gradient GEMM waits for
+  // slots an 8-40-CTA one slips into (measured: each backward split +2-7 us
+  // per step, the forward W_down / W_up+W_cgate splits -4 us)
+  for (int k = 0; k < S_COUNT; ++k) M.sk[k].S = 1;
+  plan_splits(M, {{S_ZD, B, X, H}});
+  plan_splits(M, {{S_INNER, B, H, X}, {S_CPRE, B, H, H}});
   M.lr = m->cfg.lr;
   M.beta1 = m->cfg.beta1;
   M.beta2 = m->cfg.beta2;
@@ -362,7 +409,7 @@ static int allocate(fade_model* m) {
   F(&a.h_l, B * H); F(&a.cache, B * C); F(&a.rpre, B * H);
   F(&a.ws_mem, (long long)M.splits_mem * B * H); F(&a.upre, B * H); F(&a.h_g, B * H);
   F(&a.alpha, B * H); F(&a.h_mix, B * H); F(&a.z_hat, B * H); F(&a.z_inv, B); F(&a.z, B * H);
-  F(&a.zd, B * X); F(&a.u, B * X); F(&a.inner, B * H); F(&a.cpre, B * H); F(&a.gate, B * H);
+  F(&a.zd, B * X); F(&a.u, B * X); F(&a.inner, B * H); F(&a.gate, B * H);
   F(&a.h_c, B * H); F(&a.z2_hat, B * H); F(&a.z2_inv, B); F(&a.z2, B * H);
   F(&a.a12, B * 2 * Ep); F(&a.wide, B * Ep); F(&a.ws_f, (long long)M.splits_f * B * H);
   F(&a.n_hat, B * H); F(&a.n_inv, B); F(&a.nrm, B * H); F(&a.h, B * H); F(&a.logits, B * 256);
@@ -370,12 +417,13 @@ static int allocate(fade_model* m) {
   items.push_back({(void**)&a.cum, sizeof(unsigned) * 2 * (size_t)B * kCumLd});
   items.push_back({(void**)&a.nll, sizeof(double) * (size_t)B});
   F(&a.alpha_row, B * 3);
-  F(&a.dlogits, B * 256); F(&a.dh, B * H); F(&a.dhc, B * H); F(&a.dnpre, B * H);
+  F(&a.dlogits, B * 256); F(&a.dhc, B * H); F(&a.dnpre, B * H);
   F(&a.da12, B * 2 * Ep); F(&a.ws_dz2, (long long)M.splits_dz2 * B * H); F(&a.dinner, B * H);
-  F(&a.dcpre, B * H); F(&a.du, B * X); F(&a.dhm_c, B * H); F(&a.dzd, B * X); F(&a.dz, B * H);
+  F(&a.dcpre, B * H); F(&a.dzd, B * X);
   F(&a.drpre, B * H); F(&a.dupre, B * H); F(&a.dh_l, B * H); F(&a.dx_part, B * H);
-  F(&a.dx_r, B * H); F(&a.dblock, B * d.D);
   F(&a.rowred, B * m->sl.rowred);
+  const long long sk_width[S_COUNT] = {X, H, H, 256, H, X, H, H, H, d.D};
+  for (int k = 0; k < S_COUNT; ++k) F(&M.sk[k].ws, (long long)M.sk[k].S * B * sk_width[k]);
   items.push_back({(void**)&a.emb_acc, sizeof(long long) * 256 * (size_t)d.D});
   items.push_back({(void**)&m->st, sizeof(StepState)});
   items.push_back({(void**)&m->ctx_buf, (size_t)B * d.T});
@@ -768,7 +816,8 @@ int fade_model_forward_debug(fade_model_t* m, const uint8_t* ctx, const char* pa
   CK(cudaMemcpyAsync(m->cache_snap, m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
   CK(cudaMemcpyAsync(m->ctx_buf, ctx, (size_t)d.B * d.T, cudaMemcpyHostToDevice, m->s_main));
   StepIO io = api_io(m);
-  TRY(forward(m, io, false));
+  // (the head kernel reduces the logits' split-K slices into a.logits)
+  TRY(forward(m, io, true));
   CK(cudaMemcpyAsync(out, src, sizeof(float) * d.B * width, cudaMemcpyDeviceToHost, m->s_main));
   CK(cudaMemcpyAsync(m->M.a.cache, m->cache_snap, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
   CK(cudaStreamSynchronize(m->s_main));

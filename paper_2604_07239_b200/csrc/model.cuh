@@ -59,17 +59,26 @@ struct Acts {        // saved activations and gradient scratch, all [B][ld]
   float *x, *x_hat, *x_inv, *gpre, *vpre, *loc, *loc_hat, *loc_inv, *conv_pre, *h_l;
   float *cache;                 // [B][C] rolling cache (rolled in place each predict)
   float *rpre, *ws_mem, *upre, *h_g, *alpha, *h_mix, *z_hat, *z_inv, *z;
-  float *zd, *u, *inner, *cpre, *gate, *h_c, *z2_hat, *z2_inv, *z2;
+  float *zd, *u, *inner, *gate, *h_c, *z2_hat, *z2_inv, *z2;
   float *a12, *wide, *ws_f, *n_hat, *n_inv, *nrm, *h, *logits;
   double *probs;                // [B][256] (predict API only)
   unsigned *cum;                // [2][B][kCumLd] CSPP slots
   double *nll;                  // [B]
   float *alpha_row;             // [B][3] per-row router stats (sum, min, max)
   // backward
-  float *dlogits, *dh, *dhc, *dnpre, *da12, *ws_dz2, *dinner, *dcpre, *du, *dhm_c;
-  float *dzd, *dz, *drpre, *dupre, *dh_l, *dx_part, *dx_r, *dblock;
+  float *dlogits, *dhc, *dnpre, *da12, *ws_dz2, *dinner, *dcpre;
+  float *dzd, *drpre, *dupre, *dh_l, *dx_part;
   float *rowred;                // [B][rowred]
   long long* emb_acc;           // [256][D] embedding gradient, fixed point (emb_to_fixed)
+};
+
+// Split-K partial planes of the narrow GEMMs: the GEMM writes S slices of
+// [B][N] and the consuming row kernel reduces them in a fixed order
+// (split_sum), so a 8-40-tile GEMM still spreads over ~128-148 SMs.
+enum SplitId { S_ZD, S_INNER, S_CPRE, S_LOGITS, S_DH, S_DU, S_DHMC, S_DZ, S_DXR, S_DBLOCK, S_COUNT };
+struct SplitBuf {
+  float* ws;
+  int S;
 };
 
 struct ModelPtrs {   // everything a row kernel may need, passed by value
@@ -80,6 +89,7 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   Acts a;
   StepState* st;
   int splits_mem, splits_f, splits_dz2;
+  SplitBuf sk[S_COUNT];
   double lr, beta1, beta2, adam_eps;   // Adam hyperparameters (config.py:29-32)
 };
 

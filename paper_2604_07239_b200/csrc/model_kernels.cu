@@ -53,6 +53,10 @@ __device__ __forceinline__ float split_sum(const float* __restrict__ ws, long lo
   for (int s = 0; s < S; ++s) a[s & 3] += ws[s * plane + idx];
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
+// element idx of a narrow GEMM's output [B][N] (plane = B*N), reduced over its slices
+__device__ __forceinline__ float sk_sum(const SplitBuf& k, long long plane, long long idx) {
+  return split_sum(k.ws, plane, idx, k.S);
+}
 
 // LayerNorm backward over one row (ops.py:103-113): returns dx into dxs (smem or
 // regs written by caller).  g = upstream grad (smem), xhat (global row), gain.
@@ -280,7 +284,12 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_fwd(ModelPtrs M) {
   pdl_enter();
   const int X = M.d.X, b = blockIdx.x;
   extern __shared__ float zs[];
-  for (int i = threadIdx.x; i < X; i += blockDim.x) zs[i] = M.a.zd[(long long)b * X + i];
+  const long long plane = (long long)M.d.B * X;
+  for (int i = threadIdx.x; i < X; i += blockDim.x) {
+    const float v = sk_sum(M.sk[S_ZD], plane, (long long)b * X + i);
+    zs[i] = v;
+    M.a.zd[(long long)b * X + i] = v;     // kept for the W_U gradient
+  }
   __syncthreads();
   const float* W = M.w[P_W_MIX].p + (long long)b * X * X;
   for (int o = threadIdx.x; o < X; o += blockDim.x) {
@@ -304,9 +313,12 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_fwd(ModelPtrs M) {
   float* red = hc + d.H;
   const long long rH = (long long)b * d.H;
   const float lam = M.w[P_LAM_MIX].p[0];
+  const long long plane = (long long)d.B * d.H;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    const float gt = sigmoid_f(M.a.cpre[rH + j]);
-    const float v = M.a.inner[rH + j] * gt + M.a.h_mix[rH + j] * lam;
+    const float gt = sigmoid_f(sk_sum(M.sk[S_CPRE], plane, rH + j));
+    const float in = sk_sum(M.sk[S_INNER], plane, rH + j);
+    const float v = in * gt + M.a.h_mix[rH + j] * lam;
+    M.a.inner[rH + j] = in;
     M.a.gate[rH + j] = gt;
     M.a.h_c[rH + j] = v;
     hc[j] = v;
@@ -402,7 +414,8 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
   StepState* st = M.st;
   const long long col = st->col;
   if (i == 0) bad_s = 0;
-  const float lg = M.a.logits[(long long)b * kAlphabet + i];
+  const float lg = sk_sum(M.sk[S_LOGITS], (long long)M.d.B * kAlphabet, (long long)b * kAlphabet + i);
+  M.a.logits[(long long)b * kAlphabet + i] = lg;
   __syncthreads();
   if (!isfinite(lg)) atomicOr(&bad_s, 1);
   __syncthreads();
@@ -524,8 +537,9 @@ __global__ void __launch_bounds__(kRowMax, 4) k_out_bwd(ModelPtrs M) {
   float* rr = M.a.rowred + (long long)b * M.sl.rowred;
   const float lam = M.w[P_LAM_OUT].p[0];
   float lsum = 0.f;
+  const long long plane = (long long)d.B * d.H;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    const float dh = M.a.dh[rH + j];
+    const float dh = sk_sum(M.sk[S_DH], plane, rH + j);
     const float v = dh * gelu_grad_f(M.a.nrm[rH + j]);
     dn[j] = v;
     rr[M.sl.out_g + j] = v * M.a.n_hat[rH + j];
@@ -600,7 +614,8 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
   extern __shared__ float sm[];
   float* dus = sm;          // [X]
   float* zds = sm + X;      // [X]
-  for (int i = threadIdx.x; i < X; i += blockDim.x) dus[i] = M.a.du[(long long)b * X + i];
+  for (int i = threadIdx.x; i < X; i += blockDim.x)
+    dus[i] = sk_sum(M.sk[S_DU], (long long)M.d.B * X, (long long)b * X + i);
   const int i0 = blockIdx.y * kBmmRows, i1 = min(X, i0 + kBmmRows);
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) zds[i - i0] = M.a.zd[(long long)b * X + i];
   __syncthreads();
@@ -662,8 +677,9 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_bwd(ModelPtrs M) {
   float* red = dz + d.H;
   const long long rH = (long long)b * d.H;
   float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  const long long plane = (long long)d.B * d.H;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    const float v = M.a.dz[rH + j];
+    const float v = sk_sum(M.sk[S_DZ], plane, rH + j);
     dz[j] = v;
     rr[M.sl.mix_g + j] = v * M.a.z_hat[rH + j];
     rr[M.sl.mix_b + j] = v;
@@ -677,7 +693,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_bwd(ModelPtrs M) {
   const float lam_mem = M.w[P_LAM_MEM].p[0];
   float lsum = 0.f;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    const float dhm = M.a.dhc[rH + j] * lam_mix + M.a.dhm_c[rH + j] +
+    const float dhm = M.a.dhc[rH + j] * lam_mix + sk_sum(M.sk[S_DHMC], plane, rH + j) +
                       (dz[j] * g[j] - m1 - M.a.z_hat[rH + j] * m2) * inv;
     const float al = M.a.alpha[rH + j];
     const float dal = dhm * (M.a.h_g[rH + j] - M.a.h_l[rH + j]);
@@ -730,13 +746,13 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   for (int o = tid; o < d.D; o += blockDim.x) {
     const float gp = M.a.gpre[(long long)b * d.D + o];
     const float vp = M.a.vpre[(long long)b * d.D + o];
-    const float db = M.a.dblock[(long long)b * d.D + o];
+    const float db = sk_sum(M.sk[S_DBLOCK], (long long)d.B * d.D, (long long)b * d.D + o);
     dg[o] = db * vp * gelu_grad_f(gp);
     dv[o] = db * gelu_f(gp);
     xt[o] = M.a.x[rH + d.H - d.D + o];
   }
   for (int j = tid; j < d.H; j += blockDim.x) {
-    dxs[j] = M.a.dx_r[rH + j] + M.a.dx_part[rH + j];
+    dxs[j] = sk_sum(M.sk[S_DXR], (long long)d.B * d.H, rH + j) + M.a.dx_part[rH + j];
     dcv[j] = M.a.dh_l[rH + j] * gelu_grad_f(M.a.conv_pre[rH + j]);
     locs[j] = M.a.loc[rH + j];
   }

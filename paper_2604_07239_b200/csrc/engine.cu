@@ -500,29 +500,55 @@ static int fork_side(fade_model* m, int k) {
 static int backward(fade_model* m, const StepIO& io, bool grad_only, double* losses, int advance) {
   cudaStream_t s = m->s_main, side = m->s_side;
   const ModelPtrs& M = m->M;
+  // side-stream weight updates and the model-stream position after which each
+  // is forked (0 dh, 1 out_bwd, 2 dwide, 3 dz2, 4 coarse_bwd, 5 du, 6 bmm_bwd,
+  // 7 dz, 8 mix_bwd, 9 dxr, 10 trunk_bwd); earliest legal: WF 1, W12 2, WUP 6,
+  // WROUTE 8
+  static int at[4] = {2, 3, 7, 9};
+  static bool init = false;
+  if (!init) {
+    if (const char* e = getenv("FADE_SCHED")) sscanf(e, "%d,%d,%d,%d", &at[0], &at[1], &at[2], &at[3]);
+    init = true;
+  }
+  const int ids[4] = {G_WF, G_W12, G_WUP_WCGATE, G_WROUTE_WMEM};
+  int pos = 0;
+  auto sides = [&]() -> int {
+    bool forked = false;
+    for (int k = 0; k < 4; ++k) {
+      if (at[k] != pos) continue;
+      if (!forked) TRY(fork_side(m, pos % 8));
+      forked = true;
+      TRY(run_gemm(m, ids[k], side, grad_only));
+    }
+    ++pos;
+    return FADE_OK;
+  };
   // the Adam step counter and bias-correction scalars were prepared by the
   // head kernel (HeadArgs.adam_prep); the last kernel advances the column
   TRY(run_gemm(m, G_DH, s));
+  TRY(sides());
   launch_out_bwd(M, s);
+  TRY(sides());
   TRY(run_gemm(m, G_DWIDE, s));
-  TRY(fork_side(m, 1));
-  TRY(run_gemm(m, G_WF, side, grad_only));          // + W_head
+  TRY(sides());
   TRY(run_gemm(m, G_DZ2, s));
-  TRY(fork_side(m, 2));
-  TRY(run_gemm(m, G_W12, side, grad_only));
+  TRY(sides());
   launch_coarse_bwd(M, s);
+  TRY(sides());
   TRY(run_gemm(m, G_DU_DHMC, s));
+  TRY(sides());
   // fused dzd + W_U Adam (mode 3): measured faster than moving the 201 MB W_U
   // RMW to the side stream (it then contends with the critical path for HBM)
   launch_bmm_bwd(M, grad_only, 3, s);
+  TRY(sides());
   TRY(run_gemm(m, G_DZ, s));
-  TRY(fork_side(m, 4));
-  TRY(run_gemm(m, G_WUP_WCGATE, side, grad_only));  // + W_down
+  TRY(sides());
   launch_mix_bwd(M, s);
+  TRY(sides());
   TRY(run_gemm(m, G_DXR_DBLOCK, s));
-  TRY(fork_side(m, 5));
-  TRY(run_gemm(m, G_WROUTE_WMEM, side, grad_only));
+  TRY(sides());
   launch_trunk_bwd(M, io.src, io.ld_src, io.use_col, s);
+  TRY(sides());
   launch_small_adam(M, grad_only, losses, advance, s);
   CK(cudaEventRecord(m->ev_side_done, side));
   CK(cudaStreamWaitEvent(s, m->ev_side_done, 0));

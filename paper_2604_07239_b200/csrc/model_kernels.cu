@@ -280,27 +280,53 @@ void launch_mix_fwd(const ModelPtrs& M, cudaStream_t s) {
 }
 
 // per-stream persistent memory: u[b] = zd[b] @ W_U[b]  (ops.py:44-54)
-__global__ void __launch_bounds__(kBmmThreads) k_bmm_fwd(ModelPtrs M) {
+// One CTA per stream: lanes cover 4 consecutive columns (float4, a warp reads
+// whole 512-byte rows of W_U), the 8 warps each sum a contiguous 1/8 of the
+// rows with 8 row loads in flight -- the 33.5 MB W_U read is HBM-bound --
+// and the warp partials combine in a fixed order.
+constexpr int kBmmFwdWarps = 8;
+__global__ void __launch_bounds__(32 * kBmmFwdWarps, 2) k_bmm_fwd(ModelPtrs M) {
   pdl_enter();
   const int X = M.d.X, b = blockIdx.x;
-  extern __shared__ float zs[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  extern __shared__ float zs[];                 // [X] zd row, then [8][X] partial rows
+  float* part = zs + X;
   const long long plane = (long long)M.d.B * X;
   for (int i = threadIdx.x; i < X; i += blockDim.x) {
     const float v = sk_sum(M.sk[S_ZD], plane, (long long)b * X + i);
     zs[i] = v;
-    M.a.zd[(long long)b * X + i] = v;     // kept for the W_U gradient
+    M.a.zd[(long long)b * X + i] = v;             // kept for the W_U gradient
   }
   __syncthreads();
-  const float* W = M.w[P_W_MIX].p + (long long)b * X * X;
+  const int per = (X + kBmmFwdWarps - 1) / kBmmFwdWarps;
+  const int i0 = w * per, i1 = min(X, i0 + per);
+  const int X4 = X / 4;                           // X % 4 == 0 (ModelConfig.device_check)
+  const float4* W = (const float4*)(M.w[P_W_MIX].p + (long long)b * X * X);
+  for (int j4 = lane; j4 < X4; j4 += 32) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int i = i0; i < i1; ++i) {
+      const float z = zs[i];
+      const float4 w4 = W[(long long)i * X4 + j4];
+      acc.x += z * w4.x;
+      acc.y += z * w4.y;
+      acc.z += z * w4.z;
+      acc.w += z * w4.w;
+    }
+    *(float4*)(part + w * X + 4 * j4) = acc;
+  }
+  __syncthreads();
   for (int o = threadIdx.x; o < X; o += blockDim.x) {
-    float acc = 0.f;
-    for (int i = 0; i < X; ++i) acc += zs[i] * W[(long long)i * X + o];
-    M.a.u[(long long)b * X + o] = acc;
+    float u = 0.f;
+#pragma unroll
+    for (int k = 0; k < kBmmFwdWarps; ++k) u += part[k * X + o];
+    M.a.u[(long long)b * X + o] = u;
   }
 }
 
 void launch_bmm_fwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_bmm_fwd, dim3(M.d.B), dim3(kBmmThreads), sizeof(float) * M.d.X, s, M);
+  launch_pdl(k_bmm_fwd, dim3(M.d.B), dim3(32 * kBmmFwdWarps),
+             sizeof(float) * M.d.X * (1 + kBmmFwdWarps), s, M);
 }
 
 // self-gated coarse refiner + FNR LayerNorm (model.py:156-167)

@@ -751,8 +751,8 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   float* dcv = dxs + d.H;                 // [H] dconv
   float* locs = dcv + d.H;                // [H] LN_D(emb) (conv input)
   float* dls = locs + d.H;                // [H] dloc
-  float* ck = dls + d.H;                  // [K*D*D]
-  float* dg = ck + d.K * d.D * d.D;       // [D] dgpre
+  float* ck = dls + d.H;                  // [K*D][D+1]
+  float* dg = ck + d.K * d.D * (d.D + 1); // [D] dgpre
   float* dv = dg + d.D;                   // [D] dvpre
   float* xt = dv + d.D;                   // [D]
   float* red = xt + d.D;                  // [32]
@@ -763,11 +763,12 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   const long long c0 = use_col ? M.st->col - d.T : 0;
   for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
   const float* Wv = M.w[P_W_VAL].p;
-  // taps transposed to [tap][co][ci] so the input-gradient loop below reads
-  // consecutive ci across lanes (no 32-way bank conflict)
+  // taps transposed to [tap][co][ci] with a padded row (D + 1) so both this
+  // transposing store and the input-gradient loop below are bank-conflict free
+  const int ckp = d.D + 1;
   for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) {
     const int tap = j / (d.D * d.D), ci = (j / d.D) % d.D, co = j % d.D;
-    ck[(tap * d.D + co) * d.D + ci] = M.w[P_CONV_K].p[j];
+    ck[(tap * d.D + co) * ckp + ci] = M.w[P_CONV_K].p[j];
   }
   for (int o = tid; o < d.D; o += blockDim.x) {
     const float gp = M.a.gpre[(long long)b * d.D + o];
@@ -816,14 +817,38 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     for (int t = 0; t < d.T; ++t) s += dcv[t * d.D + co];
     rr[M.sl.conv_b + co] = s;
   }
-  for (int q = tid; q < d.K * d.D * d.D; q += blockDim.x) {
-    const int tap = q / (d.D * d.D), ci = (q / d.D) % d.D, co = q % d.D;
-    float s = 0.f;
-    for (int t = 0; t < d.T; ++t) {
-      const int sidx = t + tap - pad;
-      if (sidx >= 0 && sidx < d.T) s += locs[sidx * d.D + ci] * dcv[t * d.D + co];
+  if constexpr (DT > 0) {
+    // register-blocked: one (ci, co) pair per pass, its T inputs and T output
+    // gradients loaded once and reused by all K taps
+    for (int q = tid; q < DT * DT; q += blockDim.x) {
+      const int ci = q / DT, co = q % DT;
+      float l[TT], g[TT];
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        l[t] = locs[t * DT + ci];
+        g[t] = dcv[t * DT + co];
+      }
+#pragma unroll
+      for (int tap = 0; tap < KT; ++tap) {
+        float acc = 0.f;
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+          const int sidx = t + tap - KT / 2;
+          if (sidx >= 0 && sidx < TT) acc += l[sidx] * g[t];
+        }
+        rr[M.sl.conv_k + tap * DT * DT + q] = acc;
+      }
     }
-    rr[M.sl.conv_k + q] = s;
+  } else {
+    for (int q = tid; q < d.K * d.D * d.D; q += blockDim.x) {
+      const int tap = q / (d.D * d.D), ci = (q / d.D) % d.D, co = q % d.D;
+      float s = 0.f;
+      for (int t = 0; t < d.T; ++t) {
+        const int sidx = t + tap - pad;
+        if (sidx >= 0 && sidx < d.T) s += locs[sidx * d.D + ci] * dcv[t * d.D + co];
+      }
+      rr[M.sl.conv_k + q] = s;
+    }
   }
   for (int j = tid; j < d.H; j += blockDim.x) {
     const int sidx = j / d.D, ci = j % d.D;
@@ -832,7 +857,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
       const int t = sidx - tap + pad;
       if (t < 0 || t >= d.T) continue;
       float part = 0.f;
-      for (int co = 0; co < d.D; ++co) part += dcv[t * d.D + co] * ck[(tap * d.D + co) * d.D + ci];
+      for (int co = 0; co < d.D; ++co) part += dcv[t * d.D + co] * ck[(tap * d.D + co) * ckp + ci];
       acc += part;
     }
     dls[j] = acc;
@@ -876,7 +901,8 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
 void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s) {
   const Dims& d = M.d;
-  const size_t smem = sizeof(float) * (4 * d.H + d.K * d.D * d.D + 3 * d.D + 32) + sizeof(int) * d.T;
+  const size_t smem =
+      sizeof(float) * (4 * d.H + d.K * d.D * (d.D + 1) + 3 * d.D + 32) + sizeof(int) * d.T;
   if (d.D == 32 && d.T == 16 && d.K == 3)
     launch_pdl(k_trunk_bwd<32, 16, 3>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
   else

@@ -12,8 +12,10 @@
 //              Adam fused in its epilogue) on a side stream as soon as its
 //              input gradient exists and the dX GEMM that reads the old weight
 //              is done; small parameters and the embedding last.
+#include <chrono>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -59,6 +61,25 @@ enum GemmId {
 }  // namespace fade
 
 using namespace fade;
+
+// Device allocations come from the stream-ordered pool, which keeps freed
+// memory for reuse: a plain cudaFree can stall for 100+ ms (it synchronises and
+// unmaps), which showed up as a variable per-call cost in compress_bytes.
+static cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  return cudaMallocAsync(p, bytes, s);
+}
+static void dev_free(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
 
 struct fade_model {
   fade_config_t cfg;
@@ -438,8 +459,9 @@ static int allocate(fade_model* m) {
     offs.push_back(total);
     total += it.bytes;
   }
-  CK(cudaMalloc(&m->mem, total));
-  CK(cudaMemset(m->mem, 0, total));
+  CK(dev_alloc(&m->mem, total, m->s_main));
+  CK(cudaMemsetAsync(m->mem, 0, total, m->s_main));
+  CK(cudaStreamSynchronize(m->s_main));
   for (size_t k = 0; k < items.size(); ++k) *items[k].ptr = (char*)m->mem + offs[k];
 
   M.small_p = sp; M.small_m = smm; M.small_v = sv; M.small_g = sg;
@@ -653,7 +675,8 @@ int fade_model_destroy(fade_model_t* m) {
   if (!m) return FADE_OK;
   cudaSetDevice(m->device);
   cudaDeviceSynchronize();
-  cudaFree(m->mem);
+  dev_free(m->mem, m->s_main);
+  cudaStreamSynchronize(m->s_main);
   for (auto& e : m->ev) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
     cudaEventDestroy(m->ev_cum[i]);
@@ -892,7 +915,7 @@ static int coder_create(int B, long long L, cudaStream_t s, fade_coder_t** out) 
     off[i] = total;
     total += sizes[i];
   }
-  CK(cudaMalloc(&c->mem, total));
+  CK(dev_alloc(&c->mem, total, s));
   char* base = (char*)c->mem;
   c->e.low = (unsigned long long*)(base + off[0]);
   c->e.rng = (unsigned long long*)(base + off[1]);
@@ -911,7 +934,8 @@ static int coder_create(int B, long long L, cudaStream_t s, fade_coder_t** out) 
 
 int fade_coder_destroy(fade_coder_t* c) {
   if (!c) return FADE_OK;
-  cudaFree(c->mem);
+  dev_free(c->mem, c->s);
+  cudaStreamSynchronize(c->s);
   delete c;
   return FADE_OK;
 }
@@ -930,14 +954,14 @@ int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes) {
   if (total == 0) return FADE_OK;
   long long* doff = nullptr;
   uint8_t* dout = nullptr;
-  CK(cudaMalloc(&doff, sizeof(long long) * c->B));
-  CK(cudaMalloc(&dout, (size_t)total));
-  CK(cudaMemcpy(doff, off.data(), sizeof(long long) * c->B, cudaMemcpyHostToDevice));
+  CK(dev_alloc((void**)&doff, sizeof(long long) * c->B, c->s));
+  CK(dev_alloc((void**)&dout, (size_t)total, c->s));
+  CK(cudaMemcpyAsync(doff, off.data(), sizeof(long long) * c->B, cudaMemcpyHostToDevice, c->s));
   launch_compact(c->e, c->B, doff, dout, c->s);
+  CK(cudaMemcpyAsync(payload, dout, (size_t)total, cudaMemcpyDeviceToHost, c->s));
+  dev_free(doff, c->s);
+  dev_free(dout, c->s);
   CK(cudaStreamSynchronize(c->s));
-  CK(cudaMemcpy(payload, dout, (size_t)total, cudaMemcpyDeviceToHost));
-  cudaFree(doff);
-  cudaFree(dout);
   return FADE_OK;
 }
 
@@ -985,23 +1009,35 @@ int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, in
   }
   cudaStream_t s = m ? m->s_main : nullptr;
   if (m) CK(cudaSetDevice(m->device));
+  static const bool timing = getenv("FADE_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto tA = now();
+  auto stamp = [&](const char* what) {
+    if (timing) {
+      cudaDeviceSynchronize();
+      fprintf(stderr, "[fade] compress %-10s %.3f s\n", what,
+              std::chrono::duration<double>(now() - tA).count());
+    }
+  };
   const size_t nbytes = (size_t)batch * (size_t)L;
   uint8_t* dmat = nullptr;
   const uint8_t* mat = data;
   if (!on_device && nbytes) {
-    CK(cudaMalloc(&dmat, nbytes));
+    CK(dev_alloc((void**)&dmat, nbytes, s));
     CK(cudaMemcpyAsync(dmat, data, nbytes, cudaMemcpyHostToDevice, s));
     mat = dmat;
   }
+  stamp("upload");
   fade_coder_t* c = nullptr;
   TRY(coder_create(batch, L, s, &c));
   std::unique_ptr<fade_coder> guard(c);
   launch_encode_warm(c->e, batch, mat, L, warm, s);
+  stamp("coder");
   double* dloss = nullptr;
   int status = FADE_OK;
   if (m && L > warm) {
     TRY(set_col(m, warm, warm));
-    CK(cudaMalloc(&dloss, sizeof(double) * (size_t)(L - warm)));
+    CK(dev_alloc((void**)&dloss, sizeof(double) * (size_t)(L - warm), m->s_main));
     // capture one timestep into a graph, replay it L - warm times
     cudaGraph_t graph;
     cudaGraphExec_t exec;
@@ -1011,22 +1047,36 @@ int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, in
     if (status != FADE_OK) return status;
     CK(ce);
     CK(cudaGraphInstantiate(&exec, graph, 0));
+    stamp("graph");
+    const auto t0 = now();
     // the coder's column counter must start where the model does
     for (long long i = warm; i < L; ++i) CK(cudaGraphLaunch(exec, m->s_main));
+    const auto t1 = now();
     CK(cudaStreamSynchronize(m->s_main));
+    if (timing)
+      fprintf(stderr, "[fade] compress: %lld graph launches enqueued in %.3f s, done after %.3f s\n",
+              (long long)(L - warm), std::chrono::duration<double>(t1 - t0).count(),
+              std::chrono::duration<double>(now() - t0).count());
     cudaGraphExecDestroy(exec);
+    stamp("execdestroy");
     cudaGraphDestroy(graph);
+    stamp("gdestroy");
     status = check_error(m, err);
+    stamp("checkerr");
     if (status == FADE_OK && losses)
       CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)(L - warm), cudaMemcpyDeviceToHost));
-    cudaFree(dloss);
+    stamp("losses");
+    dev_free(dloss, m->s_main);
   }
+  stamp("loop");
   launch_encode_flush(c->e, batch, s);
   c->lengths.resize(batch);
   CK(cudaMemcpyAsync(c->lengths.data(), c->e.blen, sizeof(long long) * batch,
                      cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (dmat) cudaFree(dmat);
+  dev_free(dmat, s);
+  CK(cudaStreamSynchronize(s));
+  stamp("flush");
   if (status != FADE_OK) return status;
   for (int b = 0; b < batch; ++b) lengths[b] = c->lengths[b];
   *coder_out = guard.release();
@@ -1067,7 +1117,7 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
     total += sizes[i];
   }
   void* mem = nullptr;
-  CK(cudaMalloc(&mem, total));
+  CK(dev_alloc(&mem, total, s));
   char* base = (char*)mem;
   DecState ds;
   ds.payload = (const uint8_t*)(base + offs[0]);
@@ -1091,7 +1141,7 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
   double* dloss = nullptr;
   if (m && L > warm) {
     TRY(set_col(m, warm, warm));
-    CK(cudaMalloc(&dloss, sizeof(double) * (size_t)(L - warm)));
+    CK(dev_alloc((void**)&dloss, sizeof(double) * (size_t)(L - warm), m->s_main));
     StepIO io{};
     io.src = dmat;
     io.ld_src = L;
@@ -1144,8 +1194,9 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
     if (losses && dloss)
       CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)(L - warm), cudaMemcpyDeviceToHost));
   }
-  if (dloss) cudaFree(dloss);
-  cudaFree(mem);
+  if (dloss) dev_free(dloss, m->s_main);
+  dev_free(mem, s);
+  cudaStreamSynchronize(s);
   return status;
 }
 

@@ -491,6 +491,30 @@ struct StepIO {
   HeadArgs head;
 };
 
+// L2 persistence for the per-stream W_U values (33.5 MB at B = 512, read by
+// bmm_fwd and read-modify-written by bmm_bwd every step) in the persisting L2
+// carve-out: -3 us per step.  Pinning p and m (67 MB) measured +32 us (the
+// carve-out starves the other kernels' L2).  FADE_L2PIN=0/1/2 overrides.
+static int l2_pin_mode() {
+  static const int mode = getenv("FADE_L2PIN") ? atoi(getenv("FADE_L2PIN")) : 1;
+  return mode;
+}
+struct L2Pin {
+  explicit L2Pin(const fade_model* m) {
+    const int mode = l2_pin_mode();
+    if (!mode) return;
+    const Tensor4& t = m->M.w[P_W_MIX];
+    const size_t n = sizeof(float) * (size_t)m->d.B * m->d.X * m->d.X;
+    cudaAccessPolicyWindow& w = l2_window();
+    w.base_ptr = t.p;
+    w.num_bytes = mode == 2 ? (size_t)((char*)t.m - (char*)t.p) + n : n;
+    w.hitRatio = 1.0f;
+    w.hitProp = cudaAccessPropertyPersisting;
+    w.missProp = cudaAccessPropertyStreaming;
+  }
+  ~L2Pin() { l2_window().num_bytes = 0; }
+};
+
 static int forward(fade_model* m, const StepIO& io, bool with_head) {
   cudaStream_t s = m->s_main;
   const ModelPtrs& M = m->M;
@@ -498,7 +522,10 @@ static int forward(fade_model* m, const StepIO& io, bool with_head) {
   TRY(run_gemm(m, G_ROUTE_MEM, s));
   launch_mix_fwd(M, s);
   TRY(run_gemm(m, G_DOWN, s));
-  launch_bmm_fwd(M, s);
+  {
+    L2Pin pin(m);
+    launch_bmm_fwd(M, s);
+  }
   TRY(run_gemm(m, G_UP_CGATE, s));
   launch_coarse_fwd(M, s);
   TRY(run_gemm(m, G_E12, s));
@@ -563,7 +590,10 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   TRY(sides());
   // fused dzd + W_U Adam (mode 3): measured faster than moving the 201 MB W_U
   // RMW to the side stream (it then contends with the critical path for HBM)
-  launch_bmm_bwd(M, grad_only, 3, s);
+  {
+    L2Pin pin(m);
+    launch_bmm_bwd(M, grad_only, 3, s);
+  }
   TRY(sides());
   TRY(run_gemm(m, G_DZ, s));
   TRY(sides());
@@ -665,6 +695,12 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   CK(cudaEventCreateWithFlags(&m->ev_side_done, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&m->ev_coder_join, cudaEventDisableTiming));
   TRY(allocate(m.get()));
+  if (l2_pin_mode()) {
+    const size_t want = sizeof(float) * (size_t)d.B * d.X * d.X * (l2_pin_mode() == 2 ? 2 : 1);
+    int maxp = 0;
+    CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device));
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(want, (size_t)maxp)));
+  }
   TRY(build_gemms(m.get(), m->G, false));
   TRY(build_gemms(m.get(), m->Gg, true));
   *out = m.release();

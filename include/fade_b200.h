@@ -133,8 +133,9 @@ FADE_API int fade_model_loss_grads(fade_model_t* m, const uint8_t* ctx, const ui
  * (pipeline.py:193,212-213).  m may be NULL when L <= warm.
  * pipelined = 1 runs the coder on its own CUDA stream, double-buffered against
  * the model (the CSPP of pipeline.py:229-299); 0 is the serial order.  Both
- * produce identical bytes.  Outputs: lengths[B] (host) and losses[L-warm]
- * (host, may be NULL); fetch the bytes with fade_coder_fetch. */
+ * produce identical bytes.  Outputs: lengths[B] (host), losses[L-warm] and
+ * alpha[3*(L-warm)] (host, may be NULL: per-step router mean/min/max for the
+ * metrics tape, pipeline.py:162-185); fetch the bytes with fade_coder_fetch. */
 typedef struct fade_coder fade_coder_t;
 FADE_API int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, int64_t warm,
                   int on_device, int pipelined, int64_t* lengths, double* losses,
@@ -144,10 +145,11 @@ FADE_API int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes)
 FADE_API int fade_coder_destroy(fade_coder_t* c);
 
 /* Decompress (pipeline.py:310-396): payload host bytes, lengths[B] host.
- * Writes the B x L matrix to out (host) and losses[L-warm] (may be NULL). */
+ * Writes the B x L matrix to out (host), losses[L-warm] and alpha[3*(L-warm)]
+ * (each may be NULL). */
 FADE_API int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t nbytes,
                     const int64_t* lengths, int64_t L, int64_t warm, uint8_t* out,
-                    double* losses, fade_error_t* err);
+                    double* losses, double* alpha, fade_error_t* err);
 
 /* ---- measurement hooks (bench.py) ------------------------------------------ */
 

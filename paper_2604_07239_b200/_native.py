@@ -57,7 +57,7 @@ SIGNATURES = {
     "fade_compress": (i32, [vp, i32, vp, i64, i64, i32, i32, vp, vp, vp, P(vp), P(FadeError)]),
     "fade_coder_fetch": (i32, [vp, vp, i64]),
     "fade_coder_destroy": (i32, [vp]),
-    "fade_decompress": (i32, [vp, i32, vp, i64, vp, i64, i64, vp, vp, P(FadeError)]),
+    "fade_decompress": (i32, [vp, i32, vp, i64, vp, i64, i64, vp, vp, vp, P(FadeError)]),
     "fade_bench_compress_steps": (i32, [vp, vp, i64, i64, i64, P(vp), P(i32), vp]),
     "fade_model_stream": (i32, [vp, P(vp)]),
     "fade_bench_probe": (i32, [vp, i32, i32, P(f64), P(f64), P(f64)]),

@@ -485,6 +485,7 @@ static int allocate(fade_model* m) {
 // the timestep schedule
 
 struct StepIO {
+  double* alpha_tape;        // per-step router stats [steps][3] or null
   const uint8_t* src;        // context source (stream matrix or ctx buffer)
   long long ld_src;
   int use_col;               // ctx = src[b, col-T:col] (else src[b, 0:T])
@@ -603,7 +604,7 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   TRY(sides());
   launch_trunk_bwd(M, io.src, io.ld_src, io.use_col, s);
   TRY(sides());
-  launch_small_adam(M, grad_only, losses, advance, s);
+  launch_small_adam(M, grad_only, losses, io.alpha_tape, advance, s);
   CK(cudaEventRecord(m->ev_side_done, side));
   CK(cudaStreamWaitEvent(s, m->ev_side_done, 0));
   CK(cudaGetLastError());
@@ -1003,8 +1004,9 @@ int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes) {
 
 // one compression timestep; captured once into a CUDA graph and replayed
 static int compress_step(fade_model_t* m, fade_coder_t* c, const uint8_t* data, long long L,
-                         int pipelined, double* losses) {
+                         int pipelined, double* losses, double* alpha_tape = nullptr) {
   StepIO io{};
+  io.alpha_tape = alpha_tape;
   io.src = data;
   io.ld_src = L;
   io.use_col = 1;
@@ -1033,7 +1035,6 @@ static int compress_step(fade_model_t* m, fade_coder_t* c, const uint8_t* data, 
 int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, int64_t warm,
                   int on_device, int pipelined, int64_t* lengths, double* losses, double* alpha,
                   fade_coder_t** coder_out, fade_error_t* err) {
-  (void)alpha;
   *coder_out = nullptr;
   if (m && m->d.B != batch) {
     set_last_error("compress: batch does not match the model");
@@ -1074,11 +1075,13 @@ int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, in
   if (m && L > warm) {
     TRY(set_col(m, warm, warm));
     CK(dev_alloc((void**)&dloss, sizeof(double) * (size_t)(L - warm), m->s_main));
+    double* dalpha = nullptr;
+    if (alpha) CK(dev_alloc((void**)&dalpha, sizeof(double) * 3 * (size_t)(L - warm), m->s_main));
     // capture one timestep into a graph, replay it L - warm times
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
-    status = compress_step(m, c, mat, L, pipelined, dloss);
+    status = compress_step(m, c, mat, L, pipelined, dloss, dalpha);
     cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
     if (status != FADE_OK) return status;
     CK(ce);
@@ -1101,8 +1104,11 @@ int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, in
     stamp("checkerr");
     if (status == FADE_OK && losses)
       CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)(L - warm), cudaMemcpyDeviceToHost));
+    if (status == FADE_OK && alpha)
+      CK(cudaMemcpy(alpha, dalpha, sizeof(double) * 3 * (size_t)(L - warm), cudaMemcpyDeviceToHost));
     stamp("losses");
     dev_free(dloss, m->s_main);
+    dev_free(dalpha, m->s_main);
   }
   stamp("loop");
   launch_encode_flush(c->e, batch, s);
@@ -1121,7 +1127,7 @@ int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, in
 
 int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t nbytes,
                     const int64_t* lengths, int64_t L, int64_t warm, uint8_t* out, double* losses,
-                    fade_error_t* err) {
+                    double* alpha, fade_error_t* err) {
   if (m && m->d.B != batch) {
     set_last_error("decompress: batch does not match the model");
     return FADE_ERR_USAGE;
@@ -1175,10 +1181,13 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
   launch_decode_warm(ds, batch, dmat, L, warm, err_key, s);
   int status = FADE_OK;
   double* dloss = nullptr;
+  double* dalpha = nullptr;
   if (m && L > warm) {
     TRY(set_col(m, warm, warm));
     CK(dev_alloc((void**)&dloss, sizeof(double) * (size_t)(L - warm), m->s_main));
+    if (alpha) CK(dev_alloc((void**)&dalpha, sizeof(double) * 3 * (size_t)(L - warm), m->s_main));
     StepIO io{};
+    io.alpha_tape = dalpha;
     io.src = dmat;
     io.ld_src = L;
     io.use_col = 1;
@@ -1229,8 +1238,11 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
     CK(cudaMemcpy(out, dmat, (size_t)batch * (size_t)L, cudaMemcpyDeviceToHost));
     if (losses && dloss)
       CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)(L - warm), cudaMemcpyDeviceToHost));
+    if (alpha && dalpha)
+      CK(cudaMemcpy(alpha, dalpha, sizeof(double) * 3 * (size_t)(L - warm), cudaMemcpyDeviceToHost));
   }
   if (dloss) dev_free(dloss, m->s_main);
+  if (dalpha) dev_free(dalpha, m->s_main);
   dev_free(mem, s);
   cudaStreamSynchronize(s);
   return status;

@@ -129,8 +129,10 @@ void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
                       cudaStream_t s);
 // small-parameter + embedding Adam and the step loss; advance = 1 also moves
 // the step state to the next column (the last kernel of a trained step)
-void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, int advance,
-                       cudaStream_t s);
+// alpha_tape (optional): per-step router statistics (mean, min, max) at
+// [3 * (col - loss_base)], the metrics tape of pipeline.py:162-185
+void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, double* alpha_tape,
+                       int advance, cudaStream_t s);
 
 // Embedding-gradient accumulator: 2^-48 fixed point in int64.  Integer
 // addition is associative, so atomics give a bit-reproducible sum (encoder

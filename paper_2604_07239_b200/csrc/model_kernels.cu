@@ -921,8 +921,8 @@ constexpr int kColAcc = 8;
 // fixed-point accumulator (and clear it for the next step).  Last kernel of a
 // step: with `advance` it moves the step state to the next column.
 __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int grad_only,
-                                                               double* losses, int col_blocks,
-                                                               int advance) {
+                                                               double* losses, double* alpha_tape,
+                                                               int col_blocks, int advance) {
   pdl_enter();
   if ((int)blockIdx.x >= col_blocks) {
     const int q = ((int)blockIdx.x - col_blocks) * blockDim.x + threadIdx.x;
@@ -968,10 +968,30 @@ __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int 
     double l = 0.0;
     for (int b = lane; b < M.d.B; b += 32) l += M.a.nll[b];
     l = warp_sum_d(l) / (double)M.d.B;
+    // router statistics of this step's predict for the metrics tape
+    // (model.py:197-199: mean, min, max of alpha over [B, H])
+    double as = 0.0;
+    float amn = 3.4e38f, amx = -3.4e38f;
+    if (alpha_tape) {
+      for (int b = lane; b < M.d.B; b += 32) {
+        as += M.a.alpha_row[3 * b];
+        amn = fminf(amn, M.a.alpha_row[3 * b + 1]);
+        amx = fmaxf(amx, M.a.alpha_row[3 * b + 2]);
+      }
+      as = warp_sum_d(as);
+      amn = -warp_max(-amn);
+      amx = warp_max(amx);
+    }
     if (lane == 0) {
       StepState* st = M.st;
       if (!isfinite(l)) record_error(st, st->col, 0, 5);
       if (losses) losses[st->col - st->loss_base] = l;
+      if (alpha_tape) {
+        double* rec = alpha_tape + 3 * (st->col - st->loss_base);
+        rec[0] = as / ((double)M.d.B * M.d.H);
+        rec[1] = amn;
+        rec[2] = amx;
+      }
       // nothing else in this grid reads the column; the next step waits for us
       if (advance) {
         st->col += 1;
@@ -981,12 +1001,12 @@ __global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int 
   }
 }
 
-void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, int advance,
-                       cudaStream_t s) {
+void launch_small_adam(const ModelPtrs& M, int grad_only, double* losses, double* alpha_tape,
+                       int advance, cudaStream_t s) {
   const int col_blocks = cdiv(M.sl.rowred + kAlphabet, 32);
   const int emb_blocks = cdiv(kAlphabet * M.d.D, 32 * kColWarps);
   launch_pdl(k_small_adam, dim3(col_blocks + emb_blocks), dim3(32 * kColWarps), 0, s, M, grad_only,
-             losses, col_blocks, advance);
+             losses, alpha_tape, col_blocks, advance);
 }
 
 }  // namespace fade

@@ -156,20 +156,27 @@ class CompressResult:
     metrics: list | None = None
 
 
-def _metrics(phase: str, first_step: int, losses, elapsed: float, bytes_per_step: int) -> list:
+def _metrics(phase: str, first_step: int, losses, elapsed: float, bytes_per_step: int,
+             alpha=None) -> list:
     """Per-step records of the --metrics tape (pipeline.py:162-185).
 
-    Losses come from the device; the per-step wall clock is the device run's
-    elapsed time spread uniformly (the graph replay has no host-visible steps).
+    Losses and the router statistics (mean, min, max of alpha, model.py:197-199)
+    come from the device, one row per model step; the per-step wall clock is the
+    device run's elapsed time spread uniformly (the graph replay has no
+    host-visible steps).
     """
     n = len(losses)
     recs = []
     for k, loss in enumerate(losses):
         el = elapsed * (k + 1) / max(n, 1)
-        recs.append({"phase": phase, "step": first_step + k, "loss_nats": float(loss),
-                     "bits_per_byte": float(loss) / LN2, "elapsed_s": el,
-                     "kb_per_min": ((first_step + k + 1) * bytes_per_step / 1024.0)
-                     / max(el / 60.0, 1e-9)})
+        rec = {"phase": phase, "step": first_step + k, "loss_nats": float(loss),
+               "bits_per_byte": float(loss) / LN2, "elapsed_s": el,
+               "kb_per_min": ((first_step + k + 1) * bytes_per_step / 1024.0)
+               / max(el / 60.0, 1e-9)}
+        if alpha is not None:
+            rec.update(alpha_mean=float(alpha[k, 0]), alpha_min=float(alpha[k, 1]),
+                       alpha_max=float(alpha[k, 2]))
+        recs.append(rec)
     return recs
 
 
@@ -209,9 +216,11 @@ def _compress(data: bytes, cfg: ModelConfig, variant: str, pipelined: bool,
     coder = ctypes.c_void_p()
     err = _native.FadeError()
     mat = np.ascontiguousarray(mat)
+    alpha = np.zeros((max(nsteps, 1), 3), dtype=np.float64) if collect_metrics else None
     st = lib.fade_compress(model.handle if model else None, cfg.batch, mat.ctypes.data, steps,
                            warm, 0, 1 if pipelined else 0, lengths.ctypes.data, losses.ctypes.data,
-                           None, ctypes.byref(coder), ctypes.byref(err))
+                           alpha.ctypes.data if alpha is not None else None,
+                           ctypes.byref(coder), ctypes.byref(err))
     if st != 0:
         _raise_device(st, err, "fade_compress")
     try:
@@ -226,7 +235,8 @@ def _compress(data: bytes, cfg: ModelConfig, variant: str, pipelined: bool,
     elapsed = time.perf_counter() - t0
     if trace is not None:
         PingPongBuffer(trace).replay(steps)
-    metrics = (_metrics("compress", warm, loss_list, elapsed, cfg.batch)
+    metrics = (_metrics("compress", warm, loss_list, elapsed, cfg.batch,
+                        alpha if model is not None else None)
                if collect_metrics else None)
     return CompressResult(streams, cfg, part, loss_list, elapsed, metrics)
 
@@ -287,11 +297,14 @@ def run_parallel_decompress(payload: np.ndarray, offsets: np.ndarray, lengths: n
     out = np.zeros((cfg.batch, steps), dtype=np.uint8)
     nsteps = steps - warm
     losses = np.zeros(max(nsteps, 1), dtype=np.float64)
+    alpha = np.zeros((max(nsteps, 1), 3), dtype=np.float64) if collect_metrics else None
     err = _native.FadeError()
     st = _native.lib().fade_decompress(model.handle if model else None, cfg.batch,
                                        pay.ctypes.data if pay.size else None, pay.size,
                                        lengths.ctypes.data, steps, warm, out.ctypes.data,
-                                       losses.ctypes.data, ctypes.byref(err))
+                                       losses.ctypes.data,
+                                       alpha.ctypes.data if alpha is not None else None,
+                                       ctypes.byref(err))
     if st != 0:
         _raise_device(st, err, "fade_decompress")
     data = part.join(out)
@@ -299,7 +312,8 @@ def run_parallel_decompress(payload: np.ndarray, offsets: np.ndarray, lengths: n
     if want_losses:
         return data, loss_list
     if collect_metrics:
-        return data, _metrics("decompress", warm, loss_list, time.perf_counter() - t0, cfg.batch)
+        return data, _metrics("decompress", warm, loss_list, time.perf_counter() - t0, cfg.batch,
+                              alpha if model is not None else None)
     return data
 
 

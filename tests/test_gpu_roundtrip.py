@@ -129,3 +129,43 @@ def test_sharded_v2_container_round_trip():
     res = [run_pipelined_compress(data[lo:hi], cfg) for lo, hi in shard_bounds(len(data), 3)]
     blob = container.pack_shards(res, cfg)
     assert container.decompress_bytes(blob) == data
+
+
+def test_metrics_tape_router_stats():
+    """--metrics tape (pipeline.py:162-185): per-step loss and router alpha
+    statistics from the device equal a host-driven predict/train_step replay
+    (model.py:197-199), and the decoder's tape equals the encoder's."""
+    from paper_2604_07239_b200 import corpus
+    from paper_2604_07239_b200.model import Predictor
+    from paper_2604_07239_b200.pipeline import (StreamPartition, run_parallel_decompress,
+                                                run_pipelined_compress)
+    data = corpus.make_text(3000, 9)
+    cfg = tiny()
+    res = run_pipelined_compress(data, cfg, collect_metrics=True)
+    tape = res.metrics
+    assert tape and all({"alpha_mean", "alpha_min", "alpha_max"} <= set(r) for r in tape)
+    for r in tape:
+        assert 0.0 <= r["alpha_min"] <= r["alpha_mean"] <= r["alpha_max"] <= 1.0
+    # host replay of the first steps through the Predictor API
+    part = StreamPartition.from_length(len(data), res.cfg.batch)
+    mat = part.split(data)
+    m = Predictor(res.cfg)
+    T = res.cfg.ctx_len
+    for k in range(4):
+        i = T + k
+        m.predict(mat[:, i - T:i])
+        loss = m.train_step(mat[:, i])
+        a = m.alpha_stats
+        rec = tape[k]
+        assert rec["step"] == i
+        assert abs(rec["loss_nats"] - loss) < 1e-9
+        assert abs(rec["alpha_mean"] - a[0]) < 1e-6
+        assert rec["alpha_min"] == a[1] and rec["alpha_max"] == a[2]
+    lengths = np.array([len(s) for s in res.streams], dtype=np.int64)
+    offsets = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+    payload = np.frombuffer(b"".join(res.streams), np.uint8)
+    out, dtape = run_parallel_decompress(payload, offsets, lengths, res.cfg, len(data),
+                                         collect_metrics=True)
+    assert out == data
+    assert [(r["loss_nats"], r["alpha_mean"], r["alpha_min"], r["alpha_max"]) for r in dtape] == \
+        [(r["loss_nats"], r["alpha_mean"], r["alpha_min"], r["alpha_max"]) for r in tape]

@@ -92,6 +92,9 @@ FADE_API int64_t fade_decode_step(const int64_t* cum, int64_t cum_ld, const uint
 typedef struct {
   int32_t ctx_len, embed_dim, cache_dim, mix_dim, expand_dim, batch, alphabet, conv_kernel;
   double lr, beta1, beta2, adam_eps;
+  /* ablation variant (model.py:39): 0 full, 1 dual, 2 global_only, 3 local_only,
+   * 4 mixer_nogate, 5 mixer */
+  int32_t variant;
 } fade_config_t;
 
 typedef struct fade_model fade_model_t;

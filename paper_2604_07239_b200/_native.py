@@ -29,7 +29,8 @@ class FadeConfig(ctypes.Structure):
                 ("expand_dim", ctypes.c_int32), ("batch", ctypes.c_int32),
                 ("alphabet", ctypes.c_int32), ("conv_kernel", ctypes.c_int32),
                 ("lr", ctypes.c_double), ("beta1", ctypes.c_double),
-                ("beta2", ctypes.c_double), ("adam_eps", ctypes.c_double)]
+                ("beta2", ctypes.c_double), ("adam_eps", ctypes.c_double),
+                ("variant", ctypes.c_int32)]
 
 
 # name -> (restype, argtypes); must match include/fade_b200.h

@@ -275,13 +275,17 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   }
   auto b = [&](int id) { return Builder{&Gs[id], m->bn[id]}; };
   Tensor4* w = M.w;
+  // ablation variants (model.py:121-175) drop whole GEMMs; an empty launch
+  // group is a no-op
+  const VFlags vf = vflags(M.variant);
+  float* h_final = vf.fnr ? a.h : (vf.mixer ? a.h_c : a.h_mix);
   // forward
   {
     auto bl = b(G_ROUTE_MEM);
-    TRY(bl.add(gd(a.x, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, a.rpre, H)));
+    if (vf.router) TRY(bl.add(gd(a.x, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, a.rpre, H)));
     GemmDesc g = gd(a.cache, C, 0, w[P_W_MEM].p, H, 0, B, H, C, EPI_STORE, a.ws_mem, H);
     g.splits = M.splits_mem;
-    TRY(bl.add(g));
+    if (vf.global) TRY(bl.add(g));
   }
   // narrow GEMMs write split-K slices their consumer reduces (plan_splits)
   auto sk = [&](GemmDesc g, int id) {
@@ -290,32 +294,33 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     g.splits = M.sk[id].S;
     return g;
   };
-  TRY(b(G_DOWN).add(sk(gd(a.z, H, 0, w[P_W_DOWN].p, X, 0, B, X, H, EPI_STORE, nullptr, 0), S_ZD)));
-  {
+  if (vf.mixer) {
+    TRY(b(G_DOWN).add(sk(gd(a.z, H, 0, w[P_W_DOWN].p, X, 0, B, X, H, EPI_STORE, nullptr, 0), S_ZD)));
     auto bl = b(G_UP_CGATE);
     TRY(bl.add(sk(gd(a.u, X, 0, w[P_W_UP].p, H, 0, B, H, X, EPI_STORE, nullptr, 0), S_INNER)));
-    TRY(bl.add(sk(gd(a.h_mix, H, 0, w[P_W_CGATE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_CPRE)));
+    if (vf.gate)
+      TRY(bl.add(sk(gd(a.h_mix, H, 0, w[P_W_CGATE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_CPRE)));
   }
-  {
+  if (vf.fnr) {
     GemmDesc g = gd(a.z2, H, 0, w[P_W_E1].p, 2LL * Ep, 0, B, 2 * Ep, H, EPI_GEGLU, a.a12, 2LL * Ep);
     g.aux0 = a.wide;
     g.ld_aux = Ep;
     g.aux_cols = Ep;
     TRY(b(G_E12).add(g));
   }
-  {
+  if (vf.fnr) {
     GemmDesc g = gd(a.wide, Ep, 0, w[P_W_F].p, H, 0, B, H, E, EPI_STORE, a.ws_f, H);
     g.splits = M.splits_f;
     TRY(b(G_F).add(g));
   }
   {
-    GemmDesc g = sk(gd(a.h, H, 0, w[P_W_HEAD].p, 256, 0, B, 256, H, EPI_STORE, nullptr, 0), S_LOGITS);
+    GemmDesc g = sk(gd(h_final, H, 0, w[P_W_HEAD].p, 256, 0, B, 256, H, EPI_STORE, nullptr, 0), S_LOGITS);
     g.bias = w[P_B_HEAD].p;
     TRY(b(G_HEAD).add(g));
   }
   // input gradients
   TRY(b(G_DH).add(sk(gd(a.dlogits, 256, 0, w[P_W_HEAD].p, 256, 1, B, H, 256, EPI_STORE, nullptr, 0), S_DH)));
-  {
+  if (vf.fnr) {
     GemmDesc g = gd(a.dnpre, H, 0, w[P_W_F].p, H, 1, B, E, H, EPI_GEGLU_BWD, a.da12, 2LL * Ep);
     g.aux1 = a.a12;
     g.ld_aux = 2LL * Ep;
@@ -327,22 +332,25 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     Gs[G_DWIDE].prob[0].N = Ep;
     Gs[G_DWIDE].prob[0].tiles_n = cdiv(Ep, m->bn[G_DWIDE]);
   }
-  {
+  if (vf.fnr) {
     GemmDesc g = gd(a.da12, 2LL * Ep, 0, w[P_W_E1].p, 2LL * Ep, 1, B, H, 2 * Ep, EPI_STORE, a.ws_dz2, H);
     g.splits = M.splits_dz2;
     TRY(b(G_DZ2).add(g));
   }
-  {
+  if (vf.mixer) {
     auto bl = b(G_DU_DHMC);
     TRY(bl.add(sk(gd(a.dinner, H, 0, w[P_W_UP].p, H, 1, B, X, H, EPI_STORE, nullptr, 0), S_DU)));
-    TRY(bl.add(sk(gd(a.dcpre, H, 0, w[P_W_CGATE].p, H, 1, B, H, H, EPI_STORE, nullptr, 0), S_DHMC)));
+    if (vf.gate)
+      TRY(bl.add(sk(gd(a.dcpre, H, 0, w[P_W_CGATE].p, H, 1, B, H, H, EPI_STORE, nullptr, 0), S_DHMC)));
+    TRY(b(G_DZ).add(sk(gd(a.dzd, X, 0, w[P_W_DOWN].p, X, 1, B, H, X, EPI_STORE, nullptr, 0), S_DZ)));
   }
-  TRY(b(G_DZ).add(sk(gd(a.dzd, X, 0, w[P_W_DOWN].p, X, 1, B, H, X, EPI_STORE, nullptr, 0), S_DZ)));
   {
     auto bl = b(G_DXR_DBLOCK);
-    TRY(bl.add(sk(gd(a.drpre, H, 0, w[P_W_ROUTE].p, H, 1, B, H, H, EPI_STORE, nullptr, 0), S_DXR)));
-    TRY(bl.add(sk(gd(a.dupre, H, 0, w[P_W_MEM].p + (long long)(C - d.D) * H, H, 1, B, d.D, H,
-                     EPI_STORE, nullptr, 0), S_DBLOCK)));
+    if (vf.router)
+      TRY(bl.add(sk(gd(a.drpre, H, 0, w[P_W_ROUTE].p, H, 1, B, H, H, EPI_STORE, nullptr, 0), S_DXR)));
+    if (vf.global)
+      TRY(bl.add(sk(gd(a.dupre, H, 0, w[P_W_MEM].p + (long long)(C - d.D) * H, H, 1, B, d.D, H,
+                       EPI_STORE, nullptr, 0), S_DBLOCK)));
   }
   // weight gradients with the Adam step fused into the epilogue
   auto adam = [&](GemmDesc g, const Tensor4& t) {
@@ -360,20 +368,25 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   // fewer side-stream kernels (each costs a fixed ~10 us of latency)
   {
     auto bl = b(G_WF);
-    TRY(bl.add(adam(gd(a.h, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD])));
-    TRY(bl.add(adam(gd(a.wide, Ep, 1, a.dnpre, H, 0, E, H, B, EPI_ADAM, nullptr, H), w[P_W_F])));
+    TRY(bl.add(adam(gd(h_final, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD])));
+    if (vf.fnr)
+      TRY(bl.add(adam(gd(a.wide, Ep, 1, a.dnpre, H, 0, E, H, B, EPI_ADAM, nullptr, H), w[P_W_F])));
   }
-  TRY(b(G_W12).add(adam(gd(a.z2, H, 1, a.da12, 2LL * Ep, 0, H, 2 * Ep, B, EPI_ADAM, nullptr, 2LL * Ep), w[P_W_E1])));
-  {
+  if (vf.fnr)
+    TRY(b(G_W12).add(adam(gd(a.z2, H, 1, a.da12, 2LL * Ep, 0, H, 2 * Ep, B, EPI_ADAM, nullptr, 2LL * Ep), w[P_W_E1])));
+  if (vf.mixer) {
     auto bl = b(G_WUP_WCGATE);
     TRY(bl.add(adam(gd(a.u, X, 1, a.dinner, H, 0, X, H, B, EPI_ADAM, nullptr, H), w[P_W_UP])));
-    TRY(bl.add(adam(gd(a.h_mix, H, 1, a.dcpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_CGATE])));
+    if (vf.gate)
+      TRY(bl.add(adam(gd(a.h_mix, H, 1, a.dcpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_CGATE])));
     TRY(bl.add(adam(gd(a.z, H, 1, a.dzd, X, 0, H, X, B, EPI_ADAM, nullptr, X), w[P_W_DOWN])));
   }
   {
     auto bl = b(G_WROUTE_WMEM);
-    TRY(bl.add(adam(gd(a.x, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE])));
-    TRY(bl.add(adam(gd(a.cache, C, 1, a.dupre, H, 0, C, H, B, EPI_ADAM, nullptr, H), w[P_W_MEM])));
+    if (vf.router)
+      TRY(bl.add(adam(gd(a.x, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE])));
+    if (vf.global)
+      TRY(bl.add(adam(gd(a.cache, C, 1, a.dupre, H, 0, C, H, B, EPI_ADAM, nullptr, H), w[P_W_MEM])));
   }
   return FADE_OK;
 }
@@ -406,6 +419,7 @@ static int allocate(fade_model* m) {
   for (int k = 0; k < S_COUNT; ++k) M.sk[k].S = 1;
   plan_splits(M, {{S_ZD, B, X, H}});
   plan_splits(M, {{S_INNER, B, H, X}, {S_CPRE, B, H, H}});
+  M.variant = m->cfg.variant;
   M.lr = m->cfg.lr;
   M.beta1 = m->cfg.beta1;
   M.beta2 = m->cfg.beta2;
@@ -523,15 +537,16 @@ static int forward(fade_model* m, const StepIO& io, bool with_head) {
   TRY(run_gemm(m, G_ROUTE_MEM, s));
   launch_mix_fwd(M, s);
   TRY(run_gemm(m, G_DOWN, s));
-  {
+  const VFlags vf = vflags(M.variant);
+  if (vf.mixer) {
     L2Pin pin(m);
     launch_bmm_fwd(M, s);
   }
   TRY(run_gemm(m, G_UP_CGATE, s));
-  launch_coarse_fwd(M, s);
+  if (vf.mixer) launch_coarse_fwd(M, s);
   TRY(run_gemm(m, G_E12, s));
   TRY(run_gemm(m, G_F, s));
-  launch_out_fwd(M, s);
+  if (vf.fnr) launch_out_fwd(M, s);
   TRY(run_gemm(m, G_HEAD, s));
   if (with_head) launch_head(M, io.head, s);
   CK(cudaGetLastError());
@@ -577,21 +592,22 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   };
   // the Adam step counter and bias-correction scalars were prepared by the
   // head kernel (HeadArgs.adam_prep); the last kernel advances the column
+  const VFlags vf = vflags(M.variant);
   TRY(run_gemm(m, G_DH, s));
   TRY(sides());
-  launch_out_bwd(M, s);
+  if (vf.fnr) launch_out_bwd(M, s);
   TRY(sides());
   TRY(run_gemm(m, G_DWIDE, s));
   TRY(sides());
   TRY(run_gemm(m, G_DZ2, s));
   TRY(sides());
-  launch_coarse_bwd(M, s);
+  if (vf.mixer) launch_coarse_bwd(M, s);
   TRY(sides());
   TRY(run_gemm(m, G_DU_DHMC, s));
   TRY(sides());
   // fused dzd + W_U Adam (mode 3): measured faster than moving the 201 MB W_U
   // RMW to the side stream (it then contends with the critical path for HBM)
-  {
+  if (vf.mixer) {
     L2Pin pin(m);
     launch_bmm_bwd(M, grad_only, 3, s);
   }
@@ -662,6 +678,10 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
       cfg->cache_dim % cfg->embed_dim || cfg->conv_kernel % 2 == 0 || cfg->batch < 1 ||
       cfg->ctx_len < 1) {
     set_last_error("unsupported model geometry for the B200 kernels");
+    return FADE_ERR_USAGE;
+  }
+  if (cfg->variant < 0 || cfg->variant >= V_COUNT) {
+    set_last_error("unknown model variant");
     return FADE_ERR_USAGE;
   }
   std::unique_ptr<fade_model> m(new fade_model());
@@ -885,8 +905,9 @@ static const float* part_ptr(fade_model_t* m, const char* part, int* width) {
   if (p == "alpha") return a.alpha;
   if (p == "mix") return a.h_mix;
   if (p == "mixer_inner") return a.inner;
-  if (p == "coarse") return a.h_c;
-  if (p == "hidden") return a.h;
+  const VFlags vf = vflags(m->M.variant);
+  if (p == "coarse") return vf.mixer ? a.h_c : a.h_mix;
+  if (p == "hidden") return vf.fnr ? a.h : (vf.mixer ? a.h_c : a.h_mix);
   if (p == "logits") { *width = 256; return a.logits; }
   return nullptr;
 }

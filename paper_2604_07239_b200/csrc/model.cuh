@@ -14,6 +14,27 @@
 
 namespace fade {
 
+// Ablation variants (model.py:39, 121-175) in the reference's VARIANTS order.
+enum Variant { V_FULL = 0, V_DUAL, V_GLOBAL_ONLY, V_LOCAL_ONLY, V_MIXER_NOGATE, V_MIXER, V_COUNT };
+struct VFlags {
+  bool global;   // global stream + cache roll
+  bool local;    // local conv stream
+  bool router;   // sigmoid router mixing the two
+  bool mixer;    // HGR coarse refiner (LN, W_down, per-stream W_U, W_up, skip)
+  bool gate;     // the refiner's sigmoid gate (W_cgate)
+  bool fnr;      // FNR expansion (W_e1/W_e2, W_f, output LN, skip)
+};
+__host__ __device__ inline VFlags vflags(int v) {
+  VFlags f;
+  f.global = v != V_LOCAL_ONLY;
+  f.local = v != V_GLOBAL_ONLY;
+  f.router = v != V_GLOBAL_ONLY && v != V_LOCAL_ONLY;
+  f.mixer = v == V_FULL || v == V_MIXER || v == V_MIXER_NOGATE;
+  f.gate = v == V_FULL || v == V_MIXER;
+  f.fnr = v == V_FULL;
+  return f;
+}
+
 struct Dims {
   int B, T, D, H, C, X, E, Ep, K;  // streams, ctx, embed, hidden, cache, mix, expand, padded, conv
 };
@@ -83,6 +104,7 @@ struct SplitBuf {
 
 struct ModelPtrs {   // everything a row kernel may need, passed by value
   Dims d;
+  int variant;         // Variant
   SmallLayout sl;
   Tensor4 w[P_COUNT];  // for small params these point into the small arena
   float* small_p; float* small_m; float* small_v; float* small_g;

@@ -126,8 +126,10 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   if (tid == 0) M.a.x_inv[b] = inv;
   __syncthreads();
 
+  const VFlags vf = vflags(M.variant);
   // GeGLU block of the newest symbol: gelu(x_t W_gate) * (x_t W_val)
   const float* xt = xs + (d.H - d.D);
+  if (vf.global) {
   for (int o = tid; o < d.D; o += blockDim.x) {
     float g = 0.f, v = 0.f;
     for (int i = 0; i < d.D; ++i) {
@@ -161,6 +163,8 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     __syncthreads();
     for (int o = tid; o < d.D; o += blockDim.x) crow[d.C - d.D + o] = blk[o];
   }
+  }   // global stream
+  if (!vf.local) return;
 
   // local stream: per-symbol LayerNorm over D (ops.py:94-101 on (B,T,D))
   for (int t = tid; t < d.T; t += blockDim.x) {
@@ -231,25 +235,32 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
   const long long rH = (long long)b * d.H;
   const long long plane = (long long)d.B * d.H;
   const float lam = M.w[P_LAM_MEM].p[0];
+  const VFlags vf = vflags(M.variant);
   float asum = 0.f, amin = 3.4e38f, amax = -3.4e38f;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    float up = 0.f;
-    up = split_sum(M.a.ws_mem, plane, rH + j, M.splits_mem);
-    const float hg = gelu_f(up) + M.a.x[rH + j] * lam;
-    const float al = sigmoid_f(M.a.rpre[rH + j]);
-    const float hmx = al * hg + (1.0f - al) * M.a.h_l[rH + j];
-    M.a.upre[rH + j] = up;
-    M.a.h_g[rH + j] = hg;
-    M.a.alpha[rH + j] = al;
+    float hg = 0.f, hmx;
+    if (vf.global) {
+      const float up = split_sum(M.a.ws_mem, plane, rH + j, M.splits_mem);
+      hg = gelu_f(up) + M.a.x[rH + j] * lam;
+      M.a.upre[rH + j] = up;
+      M.a.h_g[rH + j] = hg;
+    }
+    if (vf.router) {
+      const float al = sigmoid_f(M.a.rpre[rH + j]);
+      hmx = al * hg + (1.0f - al) * M.a.h_l[rH + j];
+      M.a.alpha[rH + j] = al;
+      asum += al;
+      amin = fminf(amin, al);
+      amax = fmaxf(amax, al);
+    } else {
+      hmx = vf.global ? hg : M.a.h_l[rH + j];   // single-stream variants
+    }
     M.a.h_mix[rH + j] = hmx;
     hm[j] = hmx;
-    asum += al;
-    amin = fminf(amin, al);
-    amax = fmaxf(amax, al);
   }
   __syncthreads();
   // router statistics for the metrics tape (model.py:197-199)
-  {
+  if (vf.router) {
     const float s = block_sum_rt(asum, red);
     float mn = warp_max(-amin), mx = warp_max(amax);
     __shared__ float rmn[32], rmx[32];
@@ -263,6 +274,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
       M.a.alpha_row[3 * b + 2] = c;
     }
   }
+  if (!vf.mixer) return;
   float mu, inv;
   ln_stats(hm, d.H, red, &mu, &inv);
   const float* g = M.w[P_MIX_LN_G].p;
@@ -340,8 +352,10 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_fwd(ModelPtrs M) {
   const long long rH = (long long)b * d.H;
   const float lam = M.w[P_LAM_MIX].p[0];
   const long long plane = (long long)d.B * d.H;
+  const VFlags vf = vflags(M.variant);
   for (int j = tid; j < d.H; j += blockDim.x) {
-    const float gt = sigmoid_f(sk_sum(M.sk[S_CPRE], plane, rH + j));
+    // mixer_nogate: inner + skip (inner * 1 is exact)
+    const float gt = vf.gate ? sigmoid_f(sk_sum(M.sk[S_CPRE], plane, rH + j)) : 1.0f;
     const float in = sk_sum(M.sk[S_INNER], plane, rH + j);
     const float v = in * gt + M.a.h_mix[rH + j] * lam;
     M.a.inner[rH + j] = in;
@@ -349,6 +363,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_fwd(ModelPtrs M) {
     M.a.h_c[rH + j] = v;
     hc[j] = v;
   }
+  if (!vf.fnr) return;
   __syncthreads();
   float mu, inv;
   ln_stats(hc, d.H, red, &mu, &inv);
@@ -599,25 +614,30 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_bwd(ModelPtrs M) {
   const long long rH = (long long)b * d.H;
   const long long plane = (long long)d.B * d.H;
   float* rr = M.a.rowred + (long long)b * M.sl.rowred;
-  for (int j = tid; j < d.H; j += blockDim.x) {
-    float acc = 0.f;
-    acc = split_sum(M.a.ws_dz2, plane, rH + j, M.splits_dz2);
-    dz[j] = acc;
-    rr[M.sl.ref_g + j] = acc * M.a.z2_hat[rH + j];
-    rr[M.sl.ref_b + j] = acc;
-  }
-  __syncthreads();
-  float m1, m2;
+  const VFlags vf = vflags(M.variant);
+  float m1 = 0.f, m2 = 0.f, inv = 0.f;
   const float* g = M.w[P_REF_LN_G].p;
-  ln_bwd_means(dz, M.a.z2_hat + rH, g, d.H, red, &m1, &m2);
-  const float inv = M.a.z2_inv[b];
+  if (vf.fnr) {
+    for (int j = tid; j < d.H; j += blockDim.x) {
+      float acc = 0.f;
+      acc = split_sum(M.a.ws_dz2, plane, rH + j, M.splits_dz2);
+      dz[j] = acc;
+      rr[M.sl.ref_g + j] = acc * M.a.z2_hat[rH + j];
+      rr[M.sl.ref_b + j] = acc;
+    }
+    __syncthreads();
+    ln_bwd_means(dz, M.a.z2_hat + rH, g, d.H, red, &m1, &m2);
+    inv = M.a.z2_inv[b];
+  }
   float lsum = 0.f;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    const float dhc = M.a.dhc[rH + j] + (dz[j] * g[j] - m1 - M.a.z2_hat[rH + j] * m2) * inv;
+    // without the FNR, h = h_coarse and dh arrives straight from the head GEMM
+    const float dhc = vf.fnr ? M.a.dhc[rH + j] + (dz[j] * g[j] - m1 - M.a.z2_hat[rH + j] * m2) * inv
+                             : sk_sum(M.sk[S_DH], plane, rH + j);
     const float gt = M.a.gate[rH + j];
     M.a.dhc[rH + j] = dhc;
     M.a.dinner[rH + j] = dhc * gt;
-    M.a.dcpre[rH + j] = dhc * M.a.inner[rH + j] * gt * (1.0f - gt);
+    if (vf.gate) M.a.dcpre[rH + j] = dhc * M.a.inner[rH + j] * gt * (1.0f - gt);
     lsum += dhc * M.a.h_mix[rH + j];
   }
   const float ls = block_sum_rt(lsum, red);
@@ -704,32 +724,47 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_bwd(ModelPtrs M) {
   const long long rH = (long long)b * d.H;
   float* rr = M.a.rowred + (long long)b * M.sl.rowred;
   const long long plane = (long long)d.B * d.H;
-  for (int j = tid; j < d.H; j += blockDim.x) {
-    const float v = sk_sum(M.sk[S_DZ], plane, rH + j);
-    dz[j] = v;
-    rr[M.sl.mix_g + j] = v * M.a.z_hat[rH + j];
-    rr[M.sl.mix_b + j] = v;
-  }
-  __syncthreads();
-  float m1, m2;
+  const VFlags vf = vflags(M.variant);
+  float m1 = 0.f, m2 = 0.f, inv = 0.f;
   const float* g = M.w[P_MIX_LN_G].p;
-  ln_bwd_means(dz, M.a.z_hat + rH, g, d.H, red, &m1, &m2);
-  const float inv = M.a.z_inv[b];
+  if (vf.mixer) {
+    for (int j = tid; j < d.H; j += blockDim.x) {
+      const float v = sk_sum(M.sk[S_DZ], plane, rH + j);
+      dz[j] = v;
+      rr[M.sl.mix_g + j] = v * M.a.z_hat[rH + j];
+      rr[M.sl.mix_b + j] = v;
+    }
+    __syncthreads();
+    ln_bwd_means(dz, M.a.z_hat + rH, g, d.H, red, &m1, &m2);
+    inv = M.a.z_inv[b];
+  }
   const float lam_mix = M.w[P_LAM_MIX].p[0];
   const float lam_mem = M.w[P_LAM_MEM].p[0];
   float lsum = 0.f;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    const float dhm = M.a.dhc[rH + j] * lam_mix + sk_sum(M.sk[S_DHMC], plane, rH + j) +
-                      (dz[j] * g[j] - m1 - M.a.z_hat[rH + j] * m2) * inv;
-    const float al = M.a.alpha[rH + j];
-    const float dal = dhm * (M.a.h_g[rH + j] - M.a.h_l[rH + j]);
-    const float dhg = dhm * al;
-    M.a.dh_l[rH + j] = dhm * (1.0f - al);
-    M.a.drpre[rH + j] = dal * al * (1.0f - al);
-    M.a.dupre[rH + j] = dhg * gelu_grad_f(M.a.upre[rH + j]);
-    M.a.dx_part[rH + j] = dhg * lam_mem;
-    lsum += dhg * M.a.x[rH + j];
+    float dhm;
+    if (vf.mixer) {
+      const float dhmc = vf.gate ? sk_sum(M.sk[S_DHMC], plane, rH + j) : 0.f;
+      dhm = M.a.dhc[rH + j] * lam_mix + dhmc + (dz[j] * g[j] - m1 - M.a.z_hat[rH + j] * m2) * inv;
+    } else {
+      dhm = sk_sum(M.sk[S_DH], plane, rH + j);   // h = h_mix
+    }
+    float dhg = dhm, dhl = dhm;
+    if (vf.router) {
+      const float al = M.a.alpha[rH + j];
+      const float dal = dhm * (M.a.h_g[rH + j] - M.a.h_l[rH + j]);
+      dhg = dhm * al;
+      dhl = dhm * (1.0f - al);
+      M.a.drpre[rH + j] = dal * al * (1.0f - al);
+    }
+    if (vf.local) M.a.dh_l[rH + j] = dhl;
+    if (vf.global) {
+      M.a.dupre[rH + j] = dhg * gelu_grad_f(M.a.upre[rH + j]);
+      M.a.dx_part[rH + j] = dhg * lam_mem;
+      lsum += dhg * M.a.x[rH + j];
+    }
   }
+  if (!vf.global) return;
   const float ls = block_sum_rt(lsum, red);
   if (tid == 0) rr[M.sl.lam_mem] = ls;
 }
@@ -770,35 +805,46 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     const int tap = j / (d.D * d.D), ci = (j / d.D) % d.D, co = j % d.D;
     ck[(tap * d.D + co) * ckp + ci] = M.w[P_CONV_K].p[j];
   }
-  for (int o = tid; o < d.D; o += blockDim.x) {
-    const float gp = M.a.gpre[(long long)b * d.D + o];
-    const float vp = M.a.vpre[(long long)b * d.D + o];
-    const float db = sk_sum(M.sk[S_DBLOCK], (long long)d.B * d.D, (long long)b * d.D + o);
-    dg[o] = db * vp * gelu_grad_f(gp);
-    dv[o] = db * gelu_f(gp);
-    xt[o] = M.a.x[rH + d.H - d.D + o];
+  const VFlags vf = vflags(M.variant);
+  if (vf.global) {
+    for (int o = tid; o < d.D; o += blockDim.x) {
+      const float gp = M.a.gpre[(long long)b * d.D + o];
+      const float vp = M.a.vpre[(long long)b * d.D + o];
+      const float db = sk_sum(M.sk[S_DBLOCK], (long long)d.B * d.D, (long long)b * d.D + o);
+      dg[o] = db * vp * gelu_grad_f(gp);
+      dv[o] = db * gelu_f(gp);
+      xt[o] = M.a.x[rH + d.H - d.D + o];
+    }
   }
   for (int j = tid; j < d.H; j += blockDim.x) {
-    dxs[j] = sk_sum(M.sk[S_DXR], (long long)d.B * d.H, rH + j) + M.a.dx_part[rH + j];
-    dcv[j] = M.a.dh_l[rH + j] * gelu_grad_f(M.a.conv_pre[rH + j]);
-    locs[j] = M.a.loc[rH + j];
-  }
-  __syncthreads();
-  // W_gate / W_val gradients (outer products) and dx_t
-  for (int q = tid; q < d.D * d.D; q += blockDim.x) {
-    const int i = q / d.D, o = q % d.D;
-    rr[M.sl.w_gate + q] = xt[i] * dg[o];
-    rr[M.sl.w_val + q] = xt[i] * dv[o];
-  }
-  for (int i = tid; i < d.D; i += blockDim.x) {
-    float a1 = 0.f, a2 = 0.f;
-    for (int o = 0; o < d.D; ++o) {
-      a1 += dg[o] * Wg[i * d.D + o];
-      a2 += dv[o] * Wv[i * d.D + o];
+    // dx: router (x W_route) + global skip (lam_mem x); zero in local_only
+    float dx = 0.f;
+    if (vf.router) dx = sk_sum(M.sk[S_DXR], (long long)d.B * d.H, rH + j);
+    if (vf.global) dx = vf.router ? dx + M.a.dx_part[rH + j] : M.a.dx_part[rH + j];
+    dxs[j] = dx;
+    if (vf.local) {
+      dcv[j] = M.a.dh_l[rH + j] * gelu_grad_f(M.a.conv_pre[rH + j]);
+      locs[j] = M.a.loc[rH + j];
     }
-    dxs[d.H - d.D + i] += a1 + a2;
   }
   __syncthreads();
+  if (vf.global) {
+    // W_gate / W_val gradients (outer products) and dx_t
+    for (int q = tid; q < d.D * d.D; q += blockDim.x) {
+      const int i = q / d.D, o = q % d.D;
+      rr[M.sl.w_gate + q] = xt[i] * dg[o];
+      rr[M.sl.w_val + q] = xt[i] * dv[o];
+    }
+    for (int i = tid; i < d.D; i += blockDim.x) {
+      float a1 = 0.f, a2 = 0.f;
+      for (int o = 0; o < d.D; ++o) {
+        a1 += dg[o] * Wg[i * d.D + o];
+        a2 += dv[o] * Wv[i * d.D + o];
+      }
+      dxs[d.H - d.D + i] += a1 + a2;
+    }
+    __syncthreads();
+  }
   // input LayerNorm backward
   const float* gin = M.w[P_IN_LN_G].p;
   for (int j = tid; j < d.H; j += blockDim.x) {
@@ -810,6 +856,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   const float xinv = M.a.x_inv[b];
   for (int j = tid; j < d.H; j += blockDim.x)
     dxs[j] = (dxs[j] * gin[j] - m1 - M.a.x_hat[rH + j] * m2) * xinv;   // dxf
+  if (vf.local) {
   // conv gradients: bias, taps, input (ops.py:74-88)
   const int pad = d.K / 2;
   for (int co = tid; co < d.D; co += blockDim.x) {
@@ -885,12 +932,17 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     locs[2 * t] = s1 / (float)d.D;
     locs[2 * t + 1] = s2 / (float)d.D;
   }
+  }   // local stream
   __syncthreads();
+  const float* lg = M.w[P_LOC_LN_G].p;
   for (int j = tid; j < d.H; j += blockDim.x) {
     const int t = j / d.D, e = j % d.D;
-    const float lh = M.a.loc_hat[rH + j];
-    const float de = (dls[j] * lg[e] - locs[2 * t] - lh * locs[2 * t + 1]) *
-                     M.a.loc_inv[(long long)b * d.T + t];
+    float de = 0.f;
+    if (vf.local) {
+      const float lh = M.a.loc_hat[rH + j];
+      de = (dls[j] * lg[e] - locs[2 * t] - lh * locs[2 * t + 1]) *
+           M.a.loc_inv[(long long)b * d.T + t];
+    }
     // embedding gradient (ops.py:234-243 scatter-add): integer adds commute,
     // so the fixed-point sum is the same whatever order the rows arrive in
     atomicAdd((unsigned long long*)&M.a.emb_acc[ctx[t] * d.D + e],

@@ -16,7 +16,7 @@ extern "C" {
 
 const char* fade_last_error(void) { return last_error(); }
 
-int fade_abi_version(void) { return 1; }
+int fade_abi_version(void) { return 2; }
 
 int fade_device_count(void) {
   int n = 0;

@@ -7,9 +7,10 @@ parameters, Adam moments, the rolling cache and activations live on the device
 (one ``fade_model_t``); the host only draws the seeded initialisation with
 numpy exactly as the reference does (model.py:62-105) and uploads it.
 
-Only the ``"full"`` variant is built: the container stores no variant and the
-decoder always rebuilds ``full`` (pipeline.py:329), so the ablation variants are
-not on the coding path.
+All six variants of ``VARIANTS`` (model.py:39, 121-175) run on the device: the
+ablations skip whole kernels and GEMMs.  As in the
+reference, the container stores no variant and the decoder always rebuilds
+``full`` (pipeline.py:329), so only ``full`` containers decode.
 """
 
 from __future__ import annotations
@@ -75,10 +76,11 @@ def init_params(cfg: ModelConfig) -> dict:
     return out
 
 
-def native_config(cfg: ModelConfig) -> _native.FadeConfig:
+def native_config(cfg: ModelConfig, variant: str = "full") -> _native.FadeConfig:
     return _native.FadeConfig(cfg.ctx_len, cfg.embed_dim, cfg.cache_dim, cfg.mix_dim,
                               cfg.expand_dim, cfg.batch, cfg.alphabet, cfg.conv_kernel,
-                              cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps)
+                              cfg.lr, cfg.beta1, cfg.beta2, cfg.adam_eps,
+                              VARIANTS.index(variant))
 
 
 def _ptr(a: np.ndarray):
@@ -92,8 +94,6 @@ class Predictor:
         cfg.validate()
         if variant not in VARIANTS:
             raise UsageError(f"unknown variant {variant!r}, pick one of {VARIANTS}")
-        if variant != "full":
-            raise UsageError(f"variant {variant!r} is not built for the B200 path (only 'full')")
         cfg.device_check()
         _native.require_device()
         self.cfg = cfg
@@ -102,7 +102,7 @@ class Predictor:
         self._shapes = _shapes(cfg)
         lib = _native.lib()
         h = ctypes.c_void_p()
-        _native.check(lib.fade_model_create(ctypes.byref(native_config(cfg)), device,
+        _native.check(lib.fade_model_create(ctypes.byref(native_config(cfg, variant)), device,
                                             ctypes.byref(h)), "fade_model_create")
         self._h = h
         params = init_params(cfg)
@@ -171,7 +171,9 @@ class Predictor:
         st = _native.lib().fade_model_predict(self._h, _ptr(c), _ptr(probs), _ptr(alpha),
                                               ctypes.byref(err))
         self._raise(st, err, "predict")
-        self.alpha_stats = (float(alpha[0]), float(alpha[1]), float(alpha[2]))
+        # the single-stream variants have no router (model.py:146-151)
+        self.alpha_stats = ((float(alpha[0]), float(alpha[1]), float(alpha[2]))
+                            if self.variant not in ("global_only", "local_only") else None)
         self._live = True
         return probs
 
@@ -189,8 +191,20 @@ class Predictor:
     def forward_debug(self, ctx: np.ndarray) -> dict:
         c = self._ctx(ctx)
         parts = {}
+        v = self.variant
+        skip = set()
+        if v == "local_only":
+            skip |= {"global"}
+        if v == "global_only":
+            skip |= {"local"}
+        if v in ("global_only", "local_only"):
+            skip |= {"alpha"}
+        if v not in ("full", "mixer", "mixer_nogate"):
+            skip |= {"mixer_inner"}
         for name in ("global", "local", "alpha", "mix", "mixer_inner", "coarse", "hidden",
                      "logits"):
+            if name in skip:      # the reference's parts dict has no such key (model.py:121-175)
+                continue
             width = 256 if name == "logits" else self.cfg.hidden_dim
             out = np.empty((self.cfg.batch, width), dtype=np.float32)
             _native.check(_native.lib().fade_model_forward_debug(self._h, _ptr(c), name.encode(),

@@ -216,7 +216,8 @@ def _compress(data: bytes, cfg: ModelConfig, variant: str, pipelined: bool,
     coder = ctypes.c_void_p()
     err = _native.FadeError()
     mat = np.ascontiguousarray(mat)
-    alpha = np.zeros((max(nsteps, 1), 3), dtype=np.float64) if collect_metrics else None
+    routed = variant not in ("global_only", "local_only")   # alpha exists (model.py:146-151)
+    alpha = np.zeros((max(nsteps, 1), 3), dtype=np.float64) if collect_metrics and routed else None
     st = lib.fade_compress(model.handle if model else None, cfg.batch, mat.ctypes.data, steps,
                            warm, 0, 1 if pipelined else 0, lengths.ctypes.data, losses.ctypes.data,
                            alpha.ctypes.data if alpha is not None else None,

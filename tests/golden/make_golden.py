@@ -158,6 +158,37 @@ def gen_model(name, cfg, data, steps):
     np.savez_compressed(os.path.join(OUT, f"model_{name}.npz"), **arrays)
 
 
+def gen_variants():
+    """Ablation variants (model.py:39, 121-175): per-step probabilities, losses
+    and router stats from the seeded init, then the loss gradients."""
+    from dszip.model import VARIANTS
+    from dszip.pipeline import StreamPartition
+    cfg = ModelConfig(ctx_len=4, embed_dim=8, cache_dim=32, mix_dim=8, expand_dim=32,
+                      batch=16, workers=1, seed=9)
+    data = _corpus.make_text(16 * 200, 4)
+    mat = StreamPartition.from_length(len(data), cfg.batch).split(data)
+    t, steps = cfg.ctx_len, 12
+    arrays = {"mat": mat[:, :t + steps + 1]}
+    for v in VARIANTS:
+        model = Predictor(cfg, v)
+        probs, losses, alphas = [], [], []
+        for i in range(t, t + steps):
+            probs.append(model.predict(mat[:, i - t:i]))
+            alphas.append(model.alpha_stats if model.alpha_stats is not None else (np.nan,) * 3)
+            losses.append(model.train_step(mat[:, i]))
+        i = t + steps
+        ctx = np.ascontiguousarray(mat[:, i - t:i])
+        loss, grads = model.loss_grads(ctx, mat[:, i].astype(np.int64))
+        arrays[v + "__probs"] = np.array(probs)[:, :8].astype(np.float32)   # 8 of 16 rows
+        arrays[v + "__losses"] = np.array(losses)
+        arrays[v + "__alphas"] = np.array(alphas, dtype=np.float64)
+        arrays[v + "__gloss"] = np.float64(loss)
+        for k, g in grads.items():   # parameters a variant never touches: no gradient
+            arrays[v + "__g_" + k] = (np.zeros_like(model.params[k].data) if g is None
+                                      else np.asarray(g, dtype=np.float32))
+    np.savez_compressed(os.path.join(OUT, "variants.npz"), **arrays)
+
+
 def gen_default_digest():
     """Default config (24 M params) is too big to store: keep digests + slices."""
     cfg = ModelConfig(seed=5)
@@ -230,7 +261,8 @@ def gen_corpus_digest():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["quant", "coder", "model", "container", "corpus", "default"]
+    which = sys.argv[1:] or ["quant", "coder", "model", "container", "corpus", "default",
+                             "variants"]
     if "quant" in which:
         gen_quant()
     if "coder" in which:
@@ -246,6 +278,8 @@ if __name__ == "__main__":
         gen_model("mid", mid, _corpus.make_text(64 * 200, 12), 30)
     if "container" in which:
         gen_container()
+    if "variants" in which:
+        gen_variants()
     if "default" in which:
         gen_default_digest()
     print("golden fixtures written to", OUT)

@@ -154,4 +154,4 @@ def test_abi_library_exports_every_declared_symbol():
     missing = [s for s in declared if not hasattr(so, s)]
     assert not missing
     assert declared == set(_native.SIGNATURES)
-    assert so.fade_abi_version() == 1
+    assert so.fade_abi_version() == 2

@@ -1,0 +1,67 @@
+"""Ablation variants (model.py:39, 121-175) on the B200 vs the reference's own
+trajectories (tests/golden/variants.npz, made by tests/golden/make_golden.py):
+from the same seeded init, 12 predict/train steps -- probabilities, losses
+and router statistics per step -- then the loss gradients of every parameter.
+Tolerances are the TF32 ones of tests/test_gpu_model.py."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ("full", "dual", "global_only", "local_only", "mixer_nogate", "mixer")
+
+
+def _cfg():
+    from paper_2604_07239_b200 import ModelConfig
+    return ModelConfig(ctx_len=4, embed_dim=8, cache_dim=32, mix_dim=8, expand_dim=32,
+                       batch=16, workers=1, seed=9)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_variant_trajectory_and_grads(variant):
+    from paper_2604_07239_b200.model import PARAM_ORDER, Predictor
+    z = load_golden("variants.npz")
+    mat = z["mat"]
+    cfg = _cfg()
+    m = Predictor(cfg, variant)
+    t = cfg.ctx_len
+    ref_p, ref_l, ref_a = z[variant + "__probs"], z[variant + "__losses"], z[variant + "__alphas"]
+    for k in range(len(ref_l)):
+        i = t + k
+        p = m.predict(mat[:, i - t:i])
+        assert np.abs(p[:8] - ref_p[k]).max() < 1e-3, (variant, k)
+        if np.isnan(ref_a[k, 0]):
+            assert m.alpha_stats is None
+        else:
+            assert np.allclose(m.alpha_stats, ref_a[k], atol=1e-3), (variant, k)
+        loss = m.train_step(mat[:, i])
+        assert abs(loss - ref_l[k]) < 2e-3 * abs(ref_l[k]), (variant, k, loss, ref_l[k])
+    i = t + len(ref_l)
+    loss, grads = m.loss_grads(mat[:, i - t:i], mat[:, i])
+    assert abs(loss - float(z[variant + "__gloss"])) < 2e-3 * abs(float(z[variant + "__gloss"]))
+    for name in PARAM_ORDER:
+        ref = z[variant + "__g_" + name]
+        got = grads[name].reshape(ref.shape)
+        scale = max(np.abs(ref).max(), 1e-12)
+        if np.abs(ref).max() == 0.0:
+            assert np.abs(got).max() == 0.0, (variant, name)       # unused by this variant
+        else:
+            tol = 0.1 if ref.size == 1 else 2e-2
+            assert np.abs(got - ref).max() / scale < tol, (variant, name)
+
+
+@pytest.mark.parametrize("variant", ("dual", "global_only", "local_only", "mixer_nogate", "mixer"))
+def test_variant_compress_and_metrics(variant):
+    """run_ablation's path (bench.py:142-180): the pipelined executor compresses
+    with an ablation model; the metrics tape carries router statistics only
+    for the routed variants (model.py:146-151)."""
+    from paper_2604_07239_b200 import corpus
+    from paper_2604_07239_b200.pipeline import run_pipelined_compress
+    data = corpus.make_text(2000, 5)
+    res = run_pipelined_compress(data, _cfg(), variant=variant, collect_metrics=True)
+    assert len(res.losses) > 0 and all(np.isfinite(res.losses))
+    has_alpha = variant not in ("global_only", "local_only")
+    assert ("alpha_mean" in res.metrics[0]) == has_alpha

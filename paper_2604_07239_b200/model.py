@@ -244,9 +244,41 @@ class Predictor:
                                                             int(state["step_count"])),
                       "set_counters")
 
-    @property
-    def param_count(self) -> int:
+    def param_count(self) -> int:          # a method, as model.py:262
         return int(sum(int(np.prod(s)) for s in self._shapes.values()))
+
+    def active_param_count(self) -> int:
+        """Parameters this variant's graph reaches (model.py:265-276).  The
+        reference finds them by which tensors receive a gradient; the device
+        graph is fixed per variant, so the set is static (ACTIVE_PARAMS,
+        checked against the reference's gradients in tests/test_cpu_surface.py)."""
+        return int(sum(int(np.prod(self._shapes[n])) for n in active_params(self.variant)))
+
+
+_HEAD = ("w_head", "b_head")
+_GLOBAL = ("emb", "in_ln_g", "in_ln_b", "w_gate", "w_val", "w_mem", "lam_mem")
+_LOCAL = ("emb", "loc_ln_g", "loc_ln_b", "conv_k", "conv_b")
+_MIXER = ("mix_ln_g", "mix_ln_b", "w_down", "w_mix", "w_up", "lam_mix")
+_FNR = ("ref_ln_g", "ref_ln_b", "w_e1", "w_e2", "w_f", "out_ln_g", "out_ln_b", "lam_out")
+
+
+def active_params(variant: str) -> tuple:
+    """Parameter names a variant's forward graph reaches (model.py:121-175), in
+    PARAM_ORDER.  local_only never uses x = LN(emb), so in_ln_* are inactive."""
+    names = set(_HEAD)
+    if variant != "local_only":
+        names |= set(_GLOBAL)
+    if variant != "global_only":
+        names |= set(_LOCAL)
+    if variant not in ("global_only", "local_only"):
+        names |= {"w_route", "in_ln_g", "in_ln_b"}
+    if variant in ("full", "mixer", "mixer_nogate"):
+        names |= set(_MIXER)
+    if variant in ("full", "mixer"):
+        names.add("w_cgate")
+    if variant == "full":
+        names |= set(_FNR)
+    return tuple(n for n in PARAM_ORDER if n in names)
 
 
 def nll_report(losses) -> tuple[float, float]:

@@ -155,3 +155,22 @@ def test_abi_library_exports_every_declared_symbol():
     assert not missing
     assert declared == set(_native.SIGNATURES)
     assert so.fade_abi_version() == 2
+
+
+def test_active_params_match_reference_gradients():
+    """Each variant's active parameter set (model.active_params) is exactly the
+    set of tensors the reference gives a gradient (tests/golden/variants.npz
+    stores zeros where the reference had none)."""
+    from conftest import load_golden
+    from paper_2604_07239_b200.model import PARAM_ORDER, VARIANTS, active_params
+    z = load_golden("variants.npz")
+    for v in VARIANTS:
+        reached = {n for n in PARAM_ORDER if np.abs(z[v + "__g_" + n]).max() > 0}
+        assert set(active_params(v)) == reached, v
+
+
+def test_order0_entropy():
+    from paper_2604_07239_b200 import harness
+    assert harness.order0_entropy(bytes(range(256)) * 4) == pytest.approx(8.0)
+    assert harness.order0_entropy(b"\x00" * 100) == 0.0
+    assert harness.order0_entropy(b"") == 0.0

@@ -65,3 +65,25 @@ def test_variant_compress_and_metrics(variant):
     assert len(res.losses) > 0 and all(np.isfinite(res.losses))
     has_alpha = variant not in ("global_only", "local_only")
     assert ("alpha_mean" in res.metrics[0]) == has_alpha
+
+
+def test_run_ablation_and_sweep(tmp_path):
+    """bench.py:99-180 harnesses over the device executors."""
+    from paper_2604_07239_b200 import corpus, harness
+    from paper_2604_07239_b200.model import Predictor
+    data = corpus.make_text(3000, 6)
+    rep = harness.run_ablation(data, _cfg())
+    assert set(rep) == set(VARIANTS)
+    full_params = Predictor(_cfg()).param_count()
+    for v, r in rep.items():
+        assert r["steps"] > 0 and 0.0 < r["bits_per_byte"] < 10.0 and r["ratio"] > 0.0
+        assert 0 < r["active_params"] <= full_params
+    assert rep["full"]["active_params"] == full_params
+    paths = []
+    for k, kind in enumerate(("text", "dna")):
+        p = tmp_path / f"f{k}.bin"
+        p.write_bytes(getattr(corpus, "make_" + kind)(2500, k + 1))
+        paths.append(p)
+    sw = harness.run_sweep(paths, _cfg())
+    assert len(sw["files"]) == 2
+    assert all(0.0 <= r["score"] <= 1.0 for r in sw["files"])

@@ -264,10 +264,12 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     Gs[id].occ = 2;
   }
   // CTA pairs (cta_group::2, 256-row tiles): half the operand bytes per SM
-  // (W12 update and the GeGLU backward; measured slower for the narrower
-  // W_f / W_route / W_mem updates and the forward GEMMs)
+  // (W12 update, the GeGLU backward and dz2: -15 us per step together;
+  // neutral or slower for the narrower W_f / W_route / W_mem updates and the
+  // forward GEMMs)
   static const long pair_ids = getenv("FADE_PAIR") ? atol(getenv("FADE_PAIR"))
-                                                   : (1L << G_W12) | (1L << G_DWIDE);
+                                                   : (1L << G_W12) | (1L << G_DWIDE) |
+                                                     (1L << G_DZ2);
   for (int id = 0; id < G_COUNT; ++id) {
     if (!((pair_ids >> id) & 1) || m->bn[id] < 128) continue;
     Gs[id].pair = 2;

@@ -181,7 +181,8 @@ FADE_API int fade_bench_compress_steps(fade_model_t* m, const uint8_t* data_dev,
 /* tcgen05 TF32 GEMM on device pointers: C[M,N] = A.B; a_trans=1 means A is
  * stored [K][M]; b_trans=1 means B is stored [N][K]; splits>1 writes partial
  * slices at C + s*M*ldc.  bn is the tile width (64, 128 or 256); pair = 2
- * runs CTA pairs (tcgen05 cta_group::2, 256-row tiles; bn 128 or 256). */
+ * runs CTA pairs (tcgen05 cta_group::2, 256-row tiles; bn 128 or 256); pair | 4
+ * selects the persistent warp-specialised kernel (gemm_ws.cuh). */
 FADE_API int fade_debug_gemm(const float* A, long long lda, int a_trans, const float* B,
                              long long ldb, int b_trans, float* C, long long ldc, int M, int N,
                              int K, int splits, int bn, int pair, void* stream);

@@ -275,6 +275,15 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     Gs[id].pair = 2;
     if (Gs[id].occ == 2) m->bn[id] = 256;   // pair tiles 256 x 256 at two CTAs per SM
   }
+  // persistent warp-specialised kernel (gemm_ws.cuh) for the store/GeGLU GEMMs
+  // (the FNR expand GEMM: -2.6 us per step; neutral or slower elsewhere)
+  static const long ws_ids = getenv("FADE_WS") ? atol(getenv("FADE_WS")) : (1L << G_E12);
+  for (int id = 0; id < G_COUNT; ++id) {
+    if (!((ws_ids >> id) & 1)) continue;
+    Gs[id].ws = 1;
+    if (Gs[id].pair != 2 && m->bn[id] == 256) Gs[id].pair = 2;   // 256-wide needs pairs here
+    Gs[id].occ = 1;
+  }
   auto b = [&](int id) { return Builder{&Gs[id], m->bn[id]}; };
   Tensor4* w = M.w;
   // ablation variants (model.py:121-175) drop whole GEMMs; an empty launch

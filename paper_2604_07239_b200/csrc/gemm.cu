@@ -5,6 +5,7 @@
 
 #include "../../include/fade_b200.h"
 #include "gemm.cuh"
+#include "gemm_ws.cuh"
 
 namespace fade {
 
@@ -155,6 +156,26 @@ static int launch_cfg(GemmParams& G, cudaStream_t st) {
   return FADE_OK;
 }
 
+template <int BN, int PAIR>
+static int launch_ws(GemmParams& G, cudaStream_t st) {
+  using Cfg = WsCfg<BN, PAIR>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_gemm_ws<BN, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::kSmem);
+  });
+  FADE_CUDA_TRY(attr_err);
+  int dev = 0, sms = 148;
+  FADE_CUDA_TRY(cudaGetDevice(&dev));
+  FADE_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int units = std::min(G.total_tiles, sms / PAIR);
+  FADE_CUDA_TRY(launch_pdl_cluster(k_gemm_ws<BN, PAIR>, dim3(units * PAIR), dim3(kGemmThreads),
+                                   (size_t)Cfg::kSmem, st, PAIR, G));
+  FADE_CUDA_TRY(cudaGetLastError());
+  return FADE_OK;
+}
+
 int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   int t = 0, et = 0, out = 0;
   if (G.pair != 2) G.pair = 1;
@@ -166,6 +187,18 @@ int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   }
   G.total_tiles = t;
   if (t == 0) return FADE_OK;
+  if (G.ws) {   // persistent: STORE / GEGLU epilogues only
+    for (int q = 0; q < G.nprob; ++q)
+      if (G.prob[q].epi != EPI_STORE && G.prob[q].epi != EPI_GEGLU) {
+        set_last_error("the persistent GEMM runs only the store and GeGLU epilogues");
+        return FADE_ERR_USAGE;
+      }
+    if (BN == 256 && G.pair == 2) return launch_ws<256, 2>(G, st);
+    if (BN == 128 && G.pair == 2) return launch_ws<128, 2>(G, st);
+    if (BN == 128 && G.pair != 2) return launch_ws<128, 1>(G, st);
+    set_last_error("unsupported persistent GEMM configuration");
+    return FADE_ERR_USAGE;
+  }
   auto fits = [&](int alias_tiles) {
     if (et == 0 && out > alias_tiles) {
       set_last_error("GEMM epilogue tiles exceed the pipeline smem they alias");

@@ -32,9 +32,10 @@ int fade_debug_gemm(const float* A, long long lda, int a_trans, const float* B, 
                     int pair, void* stream) {
   GemmParams G;
   memset(&G, 0, sizeof(G));
-  G.pair = pair;
+  G.pair = pair & 3;
+  G.ws = (pair & 4) ? 1 : 0;     // bit 2: the persistent kernel
   GemmDesc d{};
-  d.pair = pair;
+  d.pair = pair & 3;
   d.A = A; d.lda = lda; d.a_trans = a_trans;
   d.B = B; d.ldb = ldb; d.b_trans = b_trans;
   d.M = M; d.N = N; d.K = K;

@@ -59,3 +59,15 @@ def test_cta_pair(bn, a_trans, b_trans):
     assert run(300, 2048, 700, a_trans, b_trans, bn=bn, pair=2) < 3e-3     # ragged M and K
     assert run(128, 512, 256, a_trans, b_trans, bn=bn, pair=2) < 3e-3      # empty second CTA rows
     assert run(512, 512, 8192, a_trans, b_trans, splits=4, bn=bn, pair=2) < 3e-3
+
+
+@pytest.mark.parametrize("bn,pair", [(256, 2), (128, 2), (128, 1)])
+@pytest.mark.parametrize("a_trans,b_trans", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_persistent_ws(bn, pair, a_trans, b_trans):
+    """Persistent warp-specialised kernel (gemm_ws.cuh): several tiles per CTA,
+    two TMEM accumulators, split-K slices and ragged edges."""
+    ws = pair | 4
+    assert run(512, 16384, 512, a_trans, b_trans, bn=bn, pair=ws) < 3e-3     # many tiles / CTA
+    assert run(300, 2048, 700, a_trans, b_trans, bn=bn, pair=ws) < 3e-3      # ragged M and K
+    assert run(128, 512, 256, a_trans, b_trans, bn=bn, pair=ws) < 3e-3
+    assert run(512, 512, 8192, a_trans, b_trans, splits=18, bn=bn, pair=ws) < 3e-3

@@ -53,6 +53,32 @@ __device__ __forceinline__ float split_sum(const float* __restrict__ ws, long lo
   for (int s = 0; s < S; ++s) a[s & 3] += ws[s * plane + idx];
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
+// Row [rH, rH + n) of S split-K planes reduced into dst (smem), bit-identical
+// to split_sum: thread group g (of 4) sums the planes s = g mod 4 in order with
+// float4 loads -- every thread of the CTA keeps loads in flight -- and the
+// four partial rows combine as (p0 + p1) + (p2 + p3).  part: [4][n] smem.
+__device__ __forceinline__ void split_row(float* dst, float* part, const float* __restrict__ ws,
+                                          long long plane, long long rH, int n, int S) {
+  const int n4 = n / 4;      // n % 4 == 0 (ModelConfig.device_check)
+  for (int idx = threadIdx.x; idx < 4 * n4; idx += blockDim.x) {
+    const int g = idx / n4, j4 = idx - g * n4;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int s = g; s < S; s += 4) {
+      const float4 v = *(const float4*)(ws + s * plane + rH + 4 * j4);
+      a.x += v.x;
+      a.y += v.y;
+      a.z += v.z;
+      a.w += v.w;
+    }
+    *(float4*)(part + g * n + 4 * j4) = a;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x)
+    dst[j] = (part[j] + part[n + j]) + (part[2 * n + j] + part[3 * n + j]);
+  __syncthreads();
+}
+
 // element idx of a narrow GEMM's output [B][N] (plane = B*N), reduced over its slices
 __device__ __forceinline__ float sk_sum(const SplitBuf& k, long long plane, long long idx) {
   return split_sum(k.ws, plane, idx, k.S);
@@ -232,15 +258,18 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
   extern __shared__ float sm[];
   float* hm = sm;            // h_mix row
   float* red = hm + d.H;
+  float* ups = red + 32;     // [H] reduced W_mem pre-activation
+  float* part = ups + d.H;   // [4][H]
   const long long rH = (long long)b * d.H;
   const long long plane = (long long)d.B * d.H;
   const float lam = M.w[P_LAM_MEM].p[0];
   const VFlags vf = vflags(M.variant);
+  if (vf.global) split_row(ups, part, M.a.ws_mem, plane, rH, d.H, M.splits_mem);
   float asum = 0.f, amin = 3.4e38f, amax = -3.4e38f;
   for (int j = tid; j < d.H; j += blockDim.x) {
     float hg = 0.f, hmx;
     if (vf.global) {
-      const float up = split_sum(M.a.ws_mem, plane, rH + j, M.splits_mem);
+      const float up = ups[j];
       hg = gelu_f(up) + M.a.x[rH + j] * lam;
       M.a.upre[rH + j] = up;
       M.a.h_g[rH + j] = hg;
@@ -288,7 +317,8 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
 }
 
 void launch_mix_fwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_mix_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_mix_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (6 * M.d.H + 32), s,
+             M);
 }
 
 // per-stream persistent memory: u[b] = zd[b] @ W_U[b]  (ops.py:44-54)
@@ -389,14 +419,10 @@ __global__ void __launch_bounds__(kRowMax, 4) k_out_fwd(ModelPtrs M) {
   extern __shared__ float sm[];
   float* np_ = sm;
   float* red = np_ + d.H;
+  float* part = red + 32;                 // [4][H]
   const long long rH = (long long)b * d.H;
   const long long plane = (long long)d.B * d.H;
-  for (int j = tid; j < d.H; j += blockDim.x) {
-    float acc = 0.f;
-    acc = split_sum(M.a.ws_f, plane, rH + j, M.splits_f);
-    np_[j] = acc;
-  }
-  __syncthreads();
+  split_row(np_, part, M.a.ws_f, plane, rH, d.H, M.splits_f);
   float mu, inv;
   ln_stats(np_, d.H, red, &mu, &inv);
   const float* g = M.w[P_OUT_LN_G].p;
@@ -413,7 +439,8 @@ __global__ void __launch_bounds__(kRowMax, 4) k_out_fwd(ModelPtrs M) {
 }
 
 void launch_out_fwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_out_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_out_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (5 * M.d.H + 32), s,
+             M);
 }
 
 // ---------------------------------------------------------------------------
@@ -611,6 +638,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_bwd(ModelPtrs M) {
   extern __shared__ float sm[];
   float* dz = sm;
   float* red = dz + d.H;
+  float* part = red + 32;    // [4][H]
   const long long rH = (long long)b * d.H;
   const long long plane = (long long)d.B * d.H;
   float* rr = M.a.rowred + (long long)b * M.sl.rowred;
@@ -618,14 +646,12 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_bwd(ModelPtrs M) {
   float m1 = 0.f, m2 = 0.f, inv = 0.f;
   const float* g = M.w[P_REF_LN_G].p;
   if (vf.fnr) {
+    split_row(dz, part, M.a.ws_dz2, plane, rH, d.H, M.splits_dz2);
     for (int j = tid; j < d.H; j += blockDim.x) {
-      float acc = 0.f;
-      acc = split_sum(M.a.ws_dz2, plane, rH + j, M.splits_dz2);
-      dz[j] = acc;
+      const float acc = dz[j];
       rr[M.sl.ref_g + j] = acc * M.a.z2_hat[rH + j];
       rr[M.sl.ref_b + j] = acc;
     }
-    __syncthreads();
     ln_bwd_means(dz, M.a.z2_hat + rH, g, d.H, red, &m1, &m2);
     inv = M.a.z2_inv[b];
   }
@@ -645,7 +671,8 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_bwd(ModelPtrs M) {
 }
 
 void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s) {
-  launch_pdl(k_coarse_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
+  launch_pdl(k_coarse_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (5 * M.d.H + 32),
+             s, M);
 }
 
 // per-stream memory backward + its Adam step in one streaming pass

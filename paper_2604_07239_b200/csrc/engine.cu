@@ -102,6 +102,7 @@ struct fade_model {
   float* w12_g = nullptr;
   bool live = false;            // a predict is pending train_step
   int launches_per_step = 0;
+  size_t l2_window_max = 0, l2_persist = 0;   // access-policy window cap, persisting carve-out
 };
 
 struct fade_coder {
@@ -534,7 +535,10 @@ struct L2Pin {
     cudaAccessPolicyWindow& w = l2_window();
     w.base_ptr = t.p;
     w.num_bytes = mode == 2 ? (size_t)((char*)t.m - (char*)t.p) + n : n;
-    w.hitRatio = 1.0f;
+    // the window is capped by the device (128 MB on B200); past the persisting
+    // carve-out only that fraction of the lines is marked persisting
+    w.num_bytes = std::min(w.num_bytes, m->l2_window_max);
+    w.hitRatio = w.num_bytes ? std::min(1.0f, (float)m->l2_persist / (float)w.num_bytes) : 0.f;
     w.hitProp = cudaAccessPropertyPersisting;
     w.missProp = cudaAccessPropertyStreaming;
   }
@@ -729,9 +733,12 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   TRY(allocate(m.get()));
   if (l2_pin_mode()) {
     const size_t want = sizeof(float) * (size_t)d.B * d.X * d.X * (l2_pin_mode() == 2 ? 2 : 1);
-    int maxp = 0;
+    int maxp = 0, maxw = 0;
     CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device));
-    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(want, (size_t)maxp)));
+    CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device));
+    m->l2_persist = std::min(want, (size_t)maxp);
+    m->l2_window_max = (size_t)maxw;
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, m->l2_persist));
   }
   TRY(build_gemms(m.get(), m->G, false));
   TRY(build_gemms(m.get(), m->Gg, true));

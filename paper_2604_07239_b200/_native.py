@@ -11,6 +11,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libfade_b200.so")
+# (FADE_LIB_PATH points at an alternative build of the same library: A/B timing)
+LIB_PATH = os.environ.get("FADE_LIB_PATH", LIB_PATH)
 
 _lib = None
 

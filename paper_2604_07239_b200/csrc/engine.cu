@@ -264,6 +264,12 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     m->bn[id] = 128;
     Gs[id].occ = 2;
   }
+  // W_route/W_mem update at 64-wide tiles: 288 CTAs fill both per-SM slots
+  // (23 -> 16 us alone, -3 us per step); W_f measured slower that way
+  static const long bn64_ids = getenv("FADE_BN64") ? atol(getenv("FADE_BN64"))
+                                                   : (1L << G_WROUTE_WMEM);
+  for (int id = 0; id < G_COUNT; ++id)
+    if ((bn64_ids >> id) & 1) m->bn[id] = 64;
   // CTA pairs (cta_group::2, 256-row tiles): half the operand bytes per SM
   // (W12 update, the GeGLU backward and dz2: -15 us per step together;
   // neutral or slower for the narrower W_f / W_route / W_mem updates and the

@@ -182,7 +182,8 @@ int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   for (int q = 0; q < G.nprob; ++q) {
     G.prob[q].tile_begin = t;
     t += G.prob[q].tiles_m * G.prob[q].tiles_n * G.prob[q].splits;
-    et = std::max(et, epi_tiles(G.prob[q].epi, BN));
+    // two-per-SM launches stream their epilogue inputs through the stages
+    et = std::max(et, G.occ == 2 ? 0 : epi_tiles(G.prob[q].epi, BN));
     out = std::max(out, epi_out_tiles(G.prob[q].epi, BN));
   }
   G.total_tiles = t;
@@ -222,6 +223,7 @@ int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   }
   if (G.occ == 2) {   // two CTAs per SM: one's epilogue overlaps the other's mainloop
     if (BN == 128 && et == 0 && fits(GemmCfg<128, 0, 2>::kAliasTiles)) return launch_cfg<128, 0, 2>(G, st);
+    if (BN == 64 && et == 0 && fits(GemmCfg<64, 0, 2>::kAliasTiles)) return launch_cfg<64, 0, 2>(G, st);
     set_last_error("unsupported 2-CTA/SM GEMM configuration");
     return FADE_ERR_USAGE;
   }

@@ -409,11 +409,19 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   return FADE_OK;
 }
 
+// FADE_DBG_SKIP (1 side-stream, 2 model-stream GEMMs) and FADE_DBG_SKIPID (a
+// bit per GemmId) drop GEMM launches to measure what each costs on the
+// critical path.  Timing experiments only: the results are wrong.
 static int run_gemm(fade_model* m, int id, cudaStream_t s, bool grad_only = false) {
   static const int dbg_skip = getenv("FADE_DBG_SKIP") ? atoi(getenv("FADE_DBG_SKIP")) : 0;
+  static const long dbg_ids = getenv("FADE_DBG_SKIPID") ? atol(getenv("FADE_DBG_SKIPID")) : 0;
+  static std::once_flag warned;
+  if (dbg_skip || dbg_ids)
+    std::call_once(warned, [] {
+      fprintf(stderr, "[fade] FADE_DBG_SKIP/FADE_DBG_SKIPID set: GEMMs are skipped, results are invalid\n");
+    });
   if ((dbg_skip & 1) && s == m->s_side) return FADE_OK;
   if ((dbg_skip & 2) && s != m->s_side) return FADE_OK;
-  static const long dbg_ids = getenv("FADE_DBG_SKIPID") ? atol(getenv("FADE_DBG_SKIPID")) : 0;
   if (dbg_ids & (1L << id)) return FADE_OK;
   return gemm_launch(grad_only ? m->Gg[id] : m->G[id], m->bn[id], s);
 }

@@ -704,6 +704,48 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
   // A CTA owns kBmmRows rows of one stream: 4x more CTAs than streams keeps
   // the HBM-bound RMW evenly spread over the 148 SMs.
   const bool do_dx = mode & 1, do_upd = mode & 2;
+  constexpr int kWarps = kBmmThreads / 32;
+  if (X4 == 32 && do_upd && !grad_only) {
+    // default geometry (X = 128: one float4 per lane per row), the training
+    // path: a warp takes R rows at a time and issues all 3R loads before any
+    // Adam arithmetic, so the HBM round trips overlap instead of serialising
+    constexpr int R = 4;
+    const float4 du4 = *(const float4*)(dus + 4 * lane);
+    for (int kb = 0; i0 + w + kb * kWarps < i1; kb += R) {
+      float4 P[R], Mm[R], V[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int i = i0 + w + (kb + k) * kWarps;
+        if (i < i1) {
+          const long long q = (long long)i * 32 + lane;
+          P[k] = Wp[q];
+          Mm[k] = Wm[q];
+          V[k] = Wv[q];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int i = i0 + w + (kb + k) * kWarps;
+        if (i >= i1) continue;
+        float4 p = P[k];
+        float acc = du4.x * p.x + du4.y * p.y + du4.z * p.z + du4.w * p.w;
+        const float zi = zds[i - i0];
+        adam_update(a, zi * du4.x, &p.x, &Mm[k].x, &V[k].x);
+        adam_update(a, zi * du4.y, &p.y, &Mm[k].y, &V[k].y);
+        adam_update(a, zi * du4.z, &p.z, &Mm[k].z, &V[k].z);
+        adam_update(a, zi * du4.w, &p.w, &Mm[k].w, &V[k].w);
+        const long long q = (long long)i * 32 + lane;
+        Wp[q] = p;
+        Wm[q] = Mm[k];
+        Wv[q] = V[k];
+        if (do_dx) {
+          acc = warp_sum(acc);
+          if (lane == 0) M.a.dzd[(long long)b * X + i] = acc;
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll 4
   for (int i = i0 + w; i < i1; i += kBmmThreads / 32) {
     float acc = 0.f;

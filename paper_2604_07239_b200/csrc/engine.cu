@@ -597,10 +597,10 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   // side-stream weight updates and the model-stream position after which each
   // is forked (0 dh, 1 out_bwd, 2 dwide, 3 dz2, 4 coarse_bwd, 5 du, 6 bmm_bwd,
   // 7 dz, 8 mix_bwd, 9 dxr, 10 trunk_bwd); earliest legal: WF 1, W12 2, WUP 6,
-  // WROUTE 8.  Forking each as early as its inputs allow measured best
-  // (417.6 us/step; WF after dz2: 423.7; W12 after bmm_bwd: 427.1; W12 after
-  // mix_bwd: 429.3) -- overlap beats serialising even HBM-bound pairs.
-  static int at[4] = {2, 3, 7, 9};
+  // WROUTE 8.  Measured (us/step): W12 after dz2 and W_f/W_head after
+  // coarse_bwd (W12 runs first) 373.6; the earliest forks (2,3,7,9) 384.5;
+  // W_f first (2,2 / 3,2) 382-386; W12 or W_f after bmm_bwd or later 382-429.
+  static int at[4] = {4, 3, 7, 9};
   static bool init = false;
   if (!init) {
     if (const char* e = getenv("FADE_SCHED")) sscanf(e, "%d,%d,%d,%d", &at[0], &at[1], &at[2], &at[3]);

@@ -232,8 +232,16 @@ def run_ours(args):
         ach, peak, unit = kk["bytes"] / (kk["ms"] / 1e3) / 1e9, hbm, "GB/s"
     else:
         ach, peak, unit = kk["flops"] / (kk["ms"] / 1e3) / 1e12, tf32, "TFLOP/s"
+    # DRAM traffic per launch from the committed ncu capture of that component
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath)).get(top)
+        if t:
+            traffic = 1e6 * (t["dram_read_mb"] + t["dram_write_mb"])
     roof = {"kernel": top, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
-            "frac": ach / peak, "traffic": None, "peak_source": src + (
+            "frac": ach / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu)",
+            "algorithmic_bytes": kk["bytes"], "peak_source": src + (
                 " (TF32 = bf16/2)" if bound == "tensor" else ""),
             "share_of_timestep": kk["ms"] / step_ms,
             "components": {k: {"ms": v["ms"], "GB/s": v["bytes"] / v["ms"] / 1e6,

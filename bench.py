@@ -277,7 +277,8 @@ def run_ours(args):
                "h2d_bytes_per_step": len(sample) + init_bytes,
                "d2h_bytes_per_step": len(blob) + 8 * cfg.batch,
                "step": f"one compress_bytes() call on a {len(sample)}-byte sample per rank "
-                       "(host input, model init upload, device loop, host container)",
+                       "(host input, model init upload, device loop, host container; the "
+                       "seeded numpy parameter draw is cached in-process after its first use)",
                "bits_per_byte": 8.0 * len(blob) / len(sample),
                "decompress_value": world * len(sample) / td / 1e6}
         dec = e2e["decompress_value"]

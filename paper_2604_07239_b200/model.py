@@ -54,8 +54,30 @@ def _shapes(cfg: ModelConfig) -> dict:
     return shapes
 
 
+_INIT_CACHE: dict = {}
+
+
 def init_params(cfg: ModelConfig) -> dict:
-    """numpy ``default_rng(seed)`` draws in the reference order (model.py:62-105)."""
+    """numpy ``default_rng(seed)`` draws in the reference order (model.py:62-105).
+
+    The draw is a pure function of the geometry and the seed and costs ~0.2 s
+    at the default size, so the last result is kept (read-only arrays) for
+    repeated ``compress_bytes`` / ``Predictor`` calls with the same config.
+    """
+    key = (cfg.ctx_len, cfg.embed_dim, cfg.cache_dim, cfg.mix_dim, cfg.expand_dim, cfg.batch,
+           cfg.alphabet, cfg.conv_kernel, cfg.seed)
+    hit = _INIT_CACHE.get(key)
+    if hit is not None:
+        return hit
+    out = _draw_params(cfg)
+    for a in out.values():
+        a.flags.writeable = False
+    _INIT_CACHE.clear()
+    _INIT_CACHE[key] = out
+    return out
+
+
+def _draw_params(cfg: ModelConfig) -> dict:
     d, h, e, m = cfg.embed_dim, cfg.hidden_dim, cfg.expand_dim, cfg.mix_dim
     stds = {"emb": 0.02, "w_gate": d ** -0.5, "w_val": d ** -0.5,
             "w_mem": cfg.cache_dim ** -0.5, "conv_k": (cfg.conv_kernel * d) ** -0.5,

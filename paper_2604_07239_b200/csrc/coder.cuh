@@ -101,7 +101,8 @@ __device__ __forceinline__ int dec_symbol(DecLane& s, const CumT& cum, const uin
 // reference: p*65536 and frac*2^40 are exact power-of-two scalings, so the
 // integer keys -- and hence the largest-remainder order -- are identical.
 struct QuantSmem {
-  long long keys[kAlphabet];
+  int hist[kAlphabet];   // radix-select digit histogram
+  int sel[3];            // selected digit, its count, remaining k
   int ired[8];
   int ired2[8];
 };
@@ -145,13 +146,67 @@ __device__ __forceinline__ int quantize_sym(double p, QuantSmem& sm, bool* bad) 
   if (deficit > 0) {
     const double fr = t - (double)(long long)t;
     const long long key = (long long)(fr * 1099511627776.0) * 256 + (kAlphabet - 1 - i);
-    sm.keys[i] = key;
-    __syncthreads();
-    // rank = number of keys below mine; keys are distinct (index in low byte)
-    int rank = 0;
-#pragma unroll 8
-    for (int j = 0; j < kAlphabet; ++j) rank += (sm.keys[j] < key) ? 1 : 0;
-    if (rank >= kAlphabet - deficit) v += 1;
+    // The reference bumps the `deficit` largest keys (rank >= 256 - deficit in
+    // its argsort; keys are distinct: index in the low byte).  Select them by
+    // an MSB-first radix select over the 48-bit keys, 8-bit digits: each pass
+    // histograms the remaining candidates' digit, one warp finds the digit
+    // holding the k-th largest, larger digits are selected, smaller dropped.
+    // It stops as soon as every remaining candidate is selected (usually
+    // after two passes) -- no 256 x 256 comparison sweep.
+    bool cand = true, sel = false;
+    for (int shift = 40; shift >= 0; shift -= 8) {
+      sm.hist[i] = 0;
+      if (i == 0 && shift == 40) sm.sel[2] = deficit;
+      __syncthreads();
+      const int dg = (int)((key >> shift) & 255);
+      if (cand) atomicAdd(&sm.hist[dg], 1);
+      __syncthreads();
+      if (i < 32) {
+        // lane L owns digits 8L..8L+7; suffix sums from the top digit down
+        const int kk = sm.sel[2];
+        int h[8], s8 = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          h[q] = sm.hist[8 * i + q];
+          s8 += h[q];
+        }
+        int x = s8;   // inclusive suffix sum over lanes >= i
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_down_sync(0xffffffffu, x, o);
+          if (i + o < 32) x += y;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, x >= kk);
+        if (i == 31 - __clz(hit)) {
+          int c = x - s8;    // candidates with a larger digit than this lane's range
+#pragma unroll
+          for (int q = 7; q >= 0; --q) {
+            if (c + h[q] >= kk) {
+              sm.sel[0] = 8 * i + q;
+              sm.sel[1] = h[q];
+              sm.sel[2] = kk - c;
+              break;
+            }
+            c += h[q];
+          }
+        }
+      }
+      __syncthreads();
+      const int dsel = sm.sel[0], cnt = sm.sel[1], kk = sm.sel[2];
+      if (cand) {
+        if (dg > dsel) {
+          sel = true;
+          cand = false;
+        } else if (dg < dsel) {
+          cand = false;
+        }
+      }
+      if (cnt == kk) {            // every candidate left is among the largest
+        if (cand) sel = true;
+        break;
+      }
+    }
+    if (sel) v += 1;
     __syncthreads();
   }
   const int zeros = block_isum256(v == 0 ? 1 : 0, sm.ired);

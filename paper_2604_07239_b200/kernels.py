@@ -34,7 +34,10 @@ def _torch():
 
 def _dev(a: np.ndarray):
     torch = _torch()
-    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    a = np.ascontiguousarray(a)
+    if not a.flags.writeable:          # torch refuses read-only numpy buffers
+        a = a.copy()
+    return torch.from_numpy(a).cuda()
 
 
 def _back(t, out: np.ndarray) -> None:

@@ -297,14 +297,6 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   // group is a no-op
   const VFlags vf = vflags(M.variant);
   float* h_final = vf.fnr ? a.h : (vf.mixer ? a.h_c : a.h_mix);
-  // forward
-  {
-    auto bl = b(G_ROUTE_MEM);
-    if (vf.router) TRY(bl.add(gd(a.x, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, a.rpre, H)));
-    GemmDesc g = gd(a.cache, C, 0, w[P_W_MEM].p, H, 0, B, H, C, EPI_STORE, a.ws_mem, H);
-    g.splits = M.splits_mem;
-    if (vf.global) TRY(bl.add(g));
-  }
   // narrow GEMMs write split-K slices their consumer reduces (plan_splits)
   auto sk = [&](GemmDesc g, int id) {
     g.C = M.sk[id].ws;
@@ -312,6 +304,15 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     g.splits = M.sk[id].S;
     return g;
   };
+  // forward
+  {
+    auto bl = b(G_ROUTE_MEM);
+    if (vf.router)
+      TRY(bl.add(sk(gd(a.x, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_RPRE)));
+    GemmDesc g = gd(a.cache, C, 0, w[P_W_MEM].p, H, 0, B, H, C, EPI_STORE, a.ws_mem, H);
+    g.splits = M.splits_mem;
+    if (vf.global) TRY(bl.add(g));
+  }
   if (vf.mixer) {
     TRY(b(G_DOWN).add(sk(gd(a.z, H, 0, w[P_W_DOWN].p, X, 0, B, X, H, EPI_STORE, nullptr, 0), S_ZD)));
     auto bl = b(G_UP_CGATE);
@@ -443,6 +444,10 @@ static int allocate(fade_model* m) {
   // slots an 8-40-CTA one slips into (measured: each backward split +2-7 us
   // per step, the forward W_down / W_up+W_cgate splits -4 us)
   for (int k = 0; k < S_COUNT; ++k) M.sk[k].S = 1;
+  // the router GEMM (K = H) shares a launch with the split-K W_mem GEMM
+  // (K = C / 16 per slice): two slices balance the two
+  static const int rsplit = getenv("FADE_RPRE_SPLIT") ? atoi(getenv("FADE_RPRE_SPLIT")) : 2;
+  M.sk[S_RPRE].S = std::max(1, rsplit);
   plan_splits(M, {{S_ZD, B, X, H}});
   plan_splits(M, {{S_INNER, B, H, X}, {S_CPRE, B, H, H}});
   M.variant = m->cfg.variant;
@@ -467,7 +472,7 @@ static int allocate(fade_model* m) {
   Acts& a = M.a;
   F(&a.x, B * H); F(&a.x_hat, B * H); F(&a.x_inv, B); F(&a.gpre, B * d.D); F(&a.vpre, B * d.D);
   F(&a.loc, B * H); F(&a.loc_hat, B * H); F(&a.loc_inv, B * d.T); F(&a.conv_pre, B * H);
-  F(&a.h_l, B * H); F(&a.cache, B * C); F(&a.rpre, B * H);
+  F(&a.h_l, B * H); F(&a.cache, B * C);
   F(&a.ws_mem, (long long)M.splits_mem * B * H); F(&a.upre, B * H); F(&a.h_g, B * H);
   F(&a.alpha, B * H); F(&a.h_mix, B * H); F(&a.z_hat, B * H); F(&a.z_inv, B); F(&a.z, B * H);
   F(&a.zd, B * X); F(&a.u, B * X); F(&a.inner, B * H); F(&a.gate, B * H);
@@ -483,7 +488,7 @@ static int allocate(fade_model* m) {
   F(&a.dcpre, B * H); F(&a.dzd, B * X);
   F(&a.drpre, B * H); F(&a.dupre, B * H); F(&a.dh_l, B * H); F(&a.dx_part, B * H);
   F(&a.rowred, B * m->sl.rowred);
-  const long long sk_width[S_COUNT] = {X, H, H, 256, H, X, H, H, H, d.D};
+  const long long sk_width[S_COUNT] = {X, H, H, 256, H, X, H, H, H, d.D, H};
   for (int k = 0; k < S_COUNT; ++k) F(&M.sk[k].ws, (long long)M.sk[k].S * B * sk_width[k]);
   items.push_back({(void**)&a.emb_acc, sizeof(long long) * 256 * (size_t)d.D});
   items.push_back({(void**)&m->st, sizeof(StepState)});

@@ -79,7 +79,7 @@ struct Acts {        // saved activations and gradient scratch, all [B][ld]
   // forward
   float *x, *x_hat, *x_inv, *gpre, *vpre, *loc, *loc_hat, *loc_inv, *conv_pre, *h_l;
   float *cache;                 // [B][C] rolling cache (rolled in place each predict)
-  float *rpre, *ws_mem, *upre, *h_g, *alpha, *h_mix, *z_hat, *z_inv, *z;
+  float *ws_mem, *upre, *h_g, *alpha, *h_mix, *z_hat, *z_inv, *z;   // router pre-activation: sk[S_RPRE]
   float *zd, *u, *inner, *gate, *h_c, *z2_hat, *z2_inv, *z2;
   float *a12, *wide, *ws_f, *n_hat, *n_inv, *nrm, *h, *logits;
   double *probs;                // [B][256] (predict API only)
@@ -96,7 +96,8 @@ struct Acts {        // saved activations and gradient scratch, all [B][ld]
 // Split-K partial planes of the narrow GEMMs: the GEMM writes S slices of
 // [B][N] and the consuming row kernel reduces them in a fixed order
 // (split_sum), so a 8-40-tile GEMM still spreads over ~128-148 SMs.
-enum SplitId { S_ZD, S_INNER, S_CPRE, S_LOGITS, S_DH, S_DU, S_DHMC, S_DZ, S_DXR, S_DBLOCK, S_COUNT };
+enum SplitId { S_ZD, S_INNER, S_CPRE, S_LOGITS, S_DH, S_DU, S_DHMC, S_DZ, S_DXR, S_DBLOCK, S_RPRE,
+               S_COUNT };
 struct SplitBuf {
   float* ws;
   int S;

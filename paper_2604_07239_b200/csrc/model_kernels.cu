@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
       M.a.h_g[rH + j] = hg;
     }
     if (vf.router) {
-      const float al = sigmoid_f(M.a.rpre[rH + j]);
+      const float al = sigmoid_f(sk_sum(M.sk[S_RPRE], plane, rH + j));
       hmx = al * hg + (1.0f - al) * M.a.h_l[rH + j];
       M.a.alpha[rH + j] = al;
       asum += al;

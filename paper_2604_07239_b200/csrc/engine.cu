@@ -194,24 +194,30 @@ struct SplitPlan {
 static void plan_splits(ModelPtrs& M, std::initializer_list<SplitPlan> group) {
   std::vector<SplitPlan> g(group);
   std::vector<int> S(g.size(), 1);
-
   auto tiles = [](const SplitPlan& p) { return (int)(cdiv(p.M, kBM) * cdiv(p.N, 64)); };
+  // slices the GEMM actually makes of kt k-tiles for a requested s (gemm_setup)
+  auto made = [](int kt, int s) { return (int)cdiv(kt, cdiv(kt, s)); };
   int total = 0;
   for (auto& p : g) total += tiles(p);
   for (;;) {
-    int best = -1;
-    int best_kt = 0;
+    // give one more slice to the problem with the longest per-CTA K, while the
+    // launch stays within one wave and every slice keeps >= 2 k-tiles
+    int best = -1, best_per = 0, best_s = 0;
     for (size_t i = 0; i < g.size(); ++i) {
       const int kt = (int)cdiv(g[i].K, kBK);
-      if (kt / (2 * S[i]) < 2 || total + tiles(g[i]) * S[i] > 148) continue;
-      if (kt / S[i] > best_kt) {
-        best_kt = kt / S[i];
+      int s = S[i] + 1;
+      while (s <= kt && made(kt, s) != s) ++s;      // next slice count the GEMM realises
+      if (s > kt || cdiv(kt, s) < 2 || total + tiles(g[i]) * (s - S[i]) > 148) continue;
+      const int per = (int)cdiv(kt, S[i]);
+      if (per > best_per) {
+        best_per = per;
         best = (int)i;
+        best_s = s;
       }
     }
     if (best < 0) break;
-    total += tiles(g[best]) * S[best];
-    S[best] *= 2;
+    total += tiles(g[best]) * (best_s - S[best]);
+    S[best] = best_s;
   }
   for (size_t i = 0; i < g.size(); ++i) M.sk[g[i].id].S = S[i];
 }

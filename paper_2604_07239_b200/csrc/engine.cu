@@ -456,6 +456,7 @@ static int allocate(fade_model* m) {
   M.sk[S_RPRE].S = std::max(1, rsplit);
   plan_splits(M, {{S_ZD, B, X, H}});
   plan_splits(M, {{S_INNER, B, H, X}, {S_CPRE, B, H, H}});
+  plan_splits(M, {{S_LOGITS, B, 256, H}});     // head GEMM: -2..5 us (dh split: +1 us)
   M.variant = m->cfg.variant;
   M.lr = m->cfg.lr;
   M.beta1 = m->cfg.beta1;

@@ -22,7 +22,17 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -s -C oracle
 
+# phase-instrumented build (globaltimer stamps in the W12 and e12 GEMMs, read
+# by tools/phase_probe.py through FADE_LIB_PATH); never the shipped library
+PROBE_OBJS := $(patsubst $(SRC_DIR)/%.cu,build/probe/%.o,$(SRCS))
+build/probe/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p build/probe
+	$(NVCC) $(NVFLAGS) -DFADE_PHASE_PROBE -dc -o $@ $< 2> build/probe/$*.ptxas.log || (cat build/probe/$*.ptxas.log; exit 1)
+build/probe/libfade_b200.so: $(PROBE_OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@ $(PROBE_OBJS)
+probe: build/probe/libfade_b200.so
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean oracle
+.PHONY: all clean oracle probe

@@ -1,6 +1,7 @@
 // Host side of the tcgen05 GEMM: TMA descriptors, tiling, split-K, launch.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/fade_b200.h"
@@ -175,6 +176,13 @@ static int launch_ws(GemmParams& G, cudaStream_t st) {
   FADE_CUDA_TRY(cudaGetLastError());
   return FADE_OK;
 }
+
+#ifdef FADE_PHASE_PROBE
+__device__ unsigned long long g_phase[2048][4];
+extern "C" __attribute__((visibility("default"))) int fade_debug_phase(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_phase, sizeof(g_phase));
+}
+#endif
 
 int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   int t = 0, et = 0, out = 0;

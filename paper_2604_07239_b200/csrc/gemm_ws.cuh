@@ -76,7 +76,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
   constexpr int S = Cfg::kStages;
   constexpr int BNL = Cfg::kBNL;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // aligned by offsetting the shared array itself (not via an integer cast), so
+  // the compiler keeps the shared state space: LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* epi_smem = smem + S * Cfg::kStageBytes;
   uint64_t* full = (uint64_t*)(epi_smem + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
@@ -123,6 +125,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
+#ifdef FADE_PHASE_PROBE
+  if (threadIdx.x == 0 && BN == 256) g_phase[1024 + blockIdx.x][0] = gtimer();
+#endif
 
   const int first = blockIdx.x / PAIR, step = gridDim.x / PAIR;
 
@@ -227,6 +232,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
         mbar_wait(&accf[buf], use & 1u);
         tc_fence_after();
       }
+#ifdef FADE_PHASE_PROBE
+      if (lead && BN == 256 && jj < 2) g_phase[1024 + blockIdx.x][1 + jj] = gtimer();
+#endif
       const uint32_t taddr = tmem + ((uint32_t)(sub * 32) << 16) + buf * BN;
       auto acc16 = [&](int col, float* v) {
         if (has) {
@@ -304,6 +312,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
       }
     }
     if (lead) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#ifdef FADE_PHASE_PROBE
+    if (lead && BN == 256) g_phase[1024 + blockIdx.x][3] = gtimer();
+#endif
   }
   tc_fence_before();
   __syncthreads();

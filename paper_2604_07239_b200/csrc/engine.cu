@@ -277,12 +277,13 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   for (int id = 0; id < G_COUNT; ++id)
     if ((bn64_ids >> id) & 1) m->bn[id] = 64;
   // CTA pairs (cta_group::2, 256-row tiles): half the operand bytes per SM
-  // (W12 update, the GeGLU backward and dz2: -15 us per step together;
+  // (W12 update, the GeGLU backward and dz2: -15 us per step together; the
+  // FNR project GEMM F (split-K 18, 144 CTAs): -1.7 us;
   // neutral or slower for the narrower W_f / W_route / W_mem updates and the
-  // forward GEMMs)
+  // other forward GEMMs)
   static const long pair_ids = getenv("FADE_PAIR") ? atol(getenv("FADE_PAIR"))
                                                    : (1L << G_W12) | (1L << G_DWIDE) |
-                                                     (1L << G_DZ2);
+                                                     (1L << G_DZ2) | (1L << G_F);
   for (int id = 0; id < G_COUNT; ++id) {
     if (!((pair_ids >> id) & 1) || m->bn[id] < 128) continue;
     Gs[id].pair = 2;
@@ -444,6 +445,7 @@ static int allocate(fade_model* m) {
   const int tiles = cdiv(B, kBM) * cdiv(H, kWideBN);
   M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
   M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
+  if (const char* e = getenv("FADE_SPLITS_F")) M.splits_f = std::max(1, atoi(e));   // experiments
   M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
   // Only the forward's narrow GEMMs split: in the backward the side stream's
   // weight updates hold most SMs, and a 128-CTA input-gradient GEMM waits for

@@ -123,14 +123,44 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   float* tinv = tmu + d.T;                // [T]
   float* red = tinv + d.T;                // [32]
   int* ctx = (int*)(red + 32);            // [T]
+  // DT > 0: the cache tail [D, C) staged for the in-place roll (16-B aligned)
+  float* cstage = (float*)(((uintptr_t)(ctx + d.T) + 15) & ~(uintptr_t)15);
 
+  const VFlags vf = vflags(M.variant);
   const long long c0 = use_col ? M.st->col - d.T : 0;
-  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
-  for (int j = tid; j < d.D * d.D; j += blockDim.x) {
-    wg[j] = M.w[P_W_GATE].p[j];
-    wv[j] = M.w[P_W_VAL].p[j];
+  float* crow = M.a.cache + (long long)b * d.C;
+  const int n4 = (d.C - d.D) / 4;        // float4 count the roll moves
+  if constexpr (DT > 0) {
+    // the roll's reads depend on nothing this kernel computes: start them
+    // first (cp.async into smem) so they land under the LayerNorm/GeGLU work
+    if (vf.global) {
+      for (int q = tid; q < n4; q += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(cstage + 4 * q)),
+                     "l"(crow + d.D + 4 * q)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
   }
-  for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) ck[j] = M.w[P_CONV_K].p[j];
+  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
+  if constexpr (DT > 0) {
+    // weights into smem as float4: at the compiled geometry (D = 32, H = 512)
+    // every small-arena offset is a multiple of 4 floats (make_small_layout)
+    const float4* g4 = (const float4*)M.w[P_W_GATE].p;
+    const float4* v4 = (const float4*)M.w[P_W_VAL].p;
+    const float4* k4 = (const float4*)M.w[P_CONV_K].p;
+    for (int j = tid; j < d.D * d.D / 4; j += blockDim.x) {
+      ((float4*)wg)[j] = g4[j];
+      ((float4*)wv)[j] = v4[j];
+    }
+    for (int j = tid; j < d.K * d.D * d.D / 4; j += blockDim.x) ((float4*)ck)[j] = k4[j];
+  } else {
+    for (int j = tid; j < d.D * d.D; j += blockDim.x) {
+      wg[j] = M.w[P_W_GATE].p[j];
+      wv[j] = M.w[P_W_VAL].p[j];
+    }
+    for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) ck[j] = M.w[P_CONV_K].p[j];
+  }
   __syncthreads();
 
   // embedding gather + input LayerNorm over the flattened window
@@ -152,10 +182,42 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   if (tid == 0) M.a.x_inv[b] = inv;
   __syncthreads();
 
-  const VFlags vf = vflags(M.variant);
   // GeGLU block of the newest symbol: gelu(x_t W_gate) * (x_t W_val)
   const float* xt = xs + (d.H - d.D);
-  if (vf.global) {
+  if constexpr (DT > 0) {
+    if (vf.global) {
+      // warp w sums inputs i in [4w, 4w + 4) for all 32 outputs (lane = o;
+      // conflict-free weight rows, broadcast x_t), then a fixed-order sum of
+      // the 8 warp partials; the staged cache tail is written back meanwhile
+      static_assert(kTrunkThreads / 32 * 4 == DT, "GeGLU split");
+      float* pg = locs;                    // [8][32] partials (locs is free until the local LN)
+      float* pv = locs + 256;
+      const int w = tid >> 5, o = tid & 31;
+      float g = 0.f, v = 0.f;
+#pragma unroll
+      for (int i = 4 * w; i < 4 * w + 4; ++i) {
+        g += xt[i] * wg[i * DT + o];
+        v += xt[i] * wv[i * DT + o];
+      }
+      pg[w * 32 + o] = g;
+      pv[w * 32 + o] = v;
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();     // partials visible; every thread's cache reads landed
+      if (tid < DT) {
+        float gs = 0.f, vs = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          gs += pg[k * 32 + tid];
+          vs += pv[k * 32 + tid];
+        }
+        M.a.gpre[(long long)b * DT + tid] = gs;
+        M.a.vpre[(long long)b * DT + tid] = vs;
+        crow[d.C - DT + tid] = gelu_f(gs) * vs;
+      }
+      for (int q = tid; q < n4; q += blockDim.x) *(float4*)(crow + 4 * q) = *(const float4*)(cstage + 4 * q);
+      __syncthreads();     // locs partials consumed
+    }
+  } else if (vf.global) {
   for (int o = tid; o < d.D; o += blockDim.x) {
     float g = 0.f, v = 0.f;
     for (int i = 0; i < d.D; ++i) {
@@ -168,8 +230,6 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   }
   // roll the cache in place: new[j] = old[j + D]; new[C-D+o] = block[o]
   {
-    float* crow = M.a.cache + (long long)b * d.C;
-    const int n4 = (d.C - d.D) / 4;      // float4 count to move
     constexpr int U = 4;
     for (int base = 0; base < n4; base += U * (int)blockDim.x) {
       float4 r[U];
@@ -193,6 +253,23 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   if (!vf.local) return;
 
   // local stream: per-symbol LayerNorm over D (ops.py:94-101 on (B,T,D))
+  if constexpr (DT > 0) {
+    // warp w normalises symbols t = w, w + 8 (lane = e): shuffle trees
+    // instead of 32-long serial sums on 16 threads
+    const int w = tid >> 5, e = tid & 31;
+#pragma unroll
+    for (int t = w; t < TT; t += kTrunkThreads / 32) {
+      const float x = es[t * DT + e];
+      const float m = warp_sum(x) / (float)DT;
+      const float c = x - m;
+      const float var = warp_sum(c * c) / (float)DT;
+      if (e == 0) {
+        tmu[t] = m;
+        tinv[t] = __fdiv_rn(1.0f, __fsqrt_rn(var + kLnEps));
+        M.a.loc_inv[(long long)b * TT + t] = tinv[t];
+      }
+    }
+  } else
   for (int t = tid; t < d.T; t += blockDim.x) {
     float s = 0.f;
     for (int e = 0; e < d.D; ++e) s += es[t * d.D + e];
@@ -221,6 +298,38 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   // same-padded conv, taps in ascending order (ops.py:57-72), then gelu
   const float* cb = M.w[P_CONV_B].p;
   const int pad = d.K / 2;
+  if constexpr (DT > 0) {
+    // 256 threads = (co, t0) with t0 < TT/2; each thread also computes
+    // t1 = t0 + TT/2 with the same taps: every kernel weight load feeds two
+    // outputs, the inputs come in as float4 warp broadcasts (same t per warp)
+    static_assert(DT == 32 && TT == 16 && kTrunkThreads == DT * TT / 2, "conv thread map");
+    const int co = tid % DT, t0 = tid / DT, t1 = t0 + TT / 2;
+    float acc0 = cb[co], acc1 = acc0;
+#pragma unroll
+    for (int tap = 0; tap < KT; ++tap) {
+      const int s0 = t0 + tap - KT / 2, s1 = t1 + tap - KT / 2;
+      const bool v0 = s0 >= 0, v1 = s1 < TT;        // s0 < TT and s1 >= 0 always hold
+      const float4* l0 = (const float4*)(locs + (v0 ? s0 : 0) * DT);
+      const float4* l1 = (const float4*)(locs + (v1 ? s1 : 0) * DT);
+      const float* kc = ck + tap * DT * DT + co;
+      float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+      for (int c4 = 0; c4 < DT / 4; ++c4) {
+        const float4 a = l0[c4], bq = l1[c4];
+        const float k0 = kc[(4 * c4) * DT], k1 = kc[(4 * c4 + 1) * DT];
+        const float k2 = kc[(4 * c4 + 2) * DT], k3 = kc[(4 * c4 + 3) * DT];
+        p0 += a.x * k0; p0 += a.y * k1; p0 += a.z * k2; p0 += a.w * k3;
+        p1 += bq.x * k0; p1 += bq.y * k1; p1 += bq.z * k2; p1 += bq.w * k3;
+      }
+      if (v0) acc0 += p0;
+      if (v1) acc1 += p1;
+    }
+    M.a.conv_pre[rH + t0 * DT + co] = acc0;
+    M.a.h_l[rH + t0 * DT + co] = gelu_f(acc0);
+    M.a.conv_pre[rH + t1 * DT + co] = acc1;
+    M.a.h_l[rH + t1 * DT + co] = gelu_f(acc1);
+    return;
+  }
   for (int j = tid; j < d.H; j += blockDim.x) {
     const int t = j / d.D, co = j % d.D;
     float acc = cb[co];
@@ -243,10 +352,16 @@ void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (3 * d.H + (2 + d.K) * d.D * d.D + d.D + 2 * d.T + 32) +
                       sizeof(int) * d.T;
-  if (d.D == 32 && d.T == 16 && d.K == 3)
-    launch_pdl(k_trunk_fwd<32, 16, 3>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
-  else
+  const size_t smem_dt = smem + 16 + sizeof(float) * (d.C - d.D);   // + the staged cache tail
+  if (d.D == 32 && d.T == 16 && d.K == 3 && smem_dt <= 56 * 1024) {
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_trunk_fwd<32, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 1024);
+    (void)attr;
+    launch_pdl(k_trunk_fwd<32, 16, 3>, dim3(d.B), dim3(kTrunkThreads), smem_dt, s, M, src, ld_src,
+               use_col);
+  } else {
     launch_pdl(k_trunk_fwd<0, 0, 0>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -966,17 +1081,45 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
       rr[M.sl.conv_k + q] = s;
     }
   }
-  for (int j = tid; j < d.H; j += blockDim.x) {
-    const int sidx = j / d.D, ci = j % d.D;
-    float acc = 0.f;
-    for (int tap = 0; tap < d.K; ++tap) {
-      const int t = sidx - tap + pad;
-      if (t < 0 || t >= d.T) continue;
-      float part = 0.f;
-      for (int co = 0; co < d.D; ++co) part += dcv[t * d.D + co] * ck[(tap * d.D + co) * ckp + ci];
-      acc += part;
+  if constexpr (DT > 0) {
+    // input gradient, two positions per thread sharing each tap weight load
+    // (s0 and s0 + TT/2, same ci); dconv rows come in as float4 broadcasts
+    const int ci = tid % DT, s0 = tid / DT, s1 = s0 + TT / 2;
+    float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+    for (int tap = 0; tap < KT; ++tap) {
+      const int t0 = s0 - tap + KT / 2, t1 = s1 - tap + KT / 2;
+      const bool v0 = t0 >= 0, v1 = t1 < TT;          // t0 < TT and t1 >= 0 always hold
+      const float4* g0 = (const float4*)(dcv + (v0 ? t0 : 0) * DT);
+      const float4* g1 = (const float4*)(dcv + (v1 ? t1 : 0) * DT);
+      const float* kk = ck + tap * DT * ckp + ci;
+      float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+      for (int c4 = 0; c4 < DT / 4; ++c4) {
+        const float4 a = g0[c4], bq = g1[c4];
+        const float k0 = kk[(4 * c4) * ckp], k1 = kk[(4 * c4 + 1) * ckp];
+        const float k2 = kk[(4 * c4 + 2) * ckp], k3 = kk[(4 * c4 + 3) * ckp];
+        p0 += a.x * k0; p0 += a.y * k1; p0 += a.z * k2; p0 += a.w * k3;
+        p1 += bq.x * k0; p1 += bq.y * k1; p1 += bq.z * k2; p1 += bq.w * k3;
+      }
+      if (v0) acc0 += p0;
+      if (v1) acc1 += p1;
     }
-    dls[j] = acc;
+    dls[s0 * DT + ci] = acc0;
+    dls[s1 * DT + ci] = acc1;
+  } else {
+    for (int j = tid; j < d.H; j += blockDim.x) {
+      const int sidx = j / d.D, ci = j % d.D;
+      float acc = 0.f;
+      for (int tap = 0; tap < d.K; ++tap) {
+        const int t = sidx - tap + pad;
+        if (t < 0 || t >= d.T) continue;
+        float part = 0.f;
+        for (int co = 0; co < d.D; ++co) part += dcv[t * d.D + co] * ck[(tap * d.D + co) * ckp + ci];
+        acc += part;
+      }
+      dls[j] = acc;
+    }
   }
   __syncthreads();
   // per-symbol LayerNorm backward over D

@@ -212,6 +212,7 @@ def run_ours(args):
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * cfg.batch * K * S / (ms_max / 1e3) / 1e6
+    lib.fade_coder_destroy(coder)
 
     # the dominant components, each timed alone on the model stream
     kernels = {}

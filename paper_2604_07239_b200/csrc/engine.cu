@@ -102,6 +102,11 @@ struct fade_model {
   float* w12_g = nullptr;
   bool live = false;            // a predict is pending train_step
   int launches_per_step = 0;
+  // fade_bench_compress_steps: the captured timestep, owned by this model (a
+  // cache keyed by the model's address replayed a destroyed model's graph when
+  // a new model reused the address) and tied to the coder it was captured with
+  cudaGraphExec_t bench_exec = nullptr;
+  const void* bench_coder = nullptr;
   size_t l2_window_max = 0, l2_persist = 0;   // access-policy window cap, persisting carve-out
 };
 
@@ -778,6 +783,7 @@ int fade_model_destroy(fade_model_t* m) {
   if (!m) return FADE_OK;
   cudaSetDevice(m->device);
   cudaDeviceSynchronize();
+  if (m->bench_exec) cudaGraphExecDestroy(m->bench_exec);
   dev_free(m->mem, m->s_main);
   cudaStreamSynchronize(m->s_main);
   for (auto& e : m->ev) cudaEventDestroy(e);
@@ -1385,23 +1391,23 @@ int fade_bench_compress_steps(fade_model_t* m, const uint8_t* data_dev, int64_t 
     long long v = start;
     CK(cudaMemcpy((*coder)->e.col, &v, sizeof(v), cudaMemcpyHostToDevice));
   }
-  static thread_local cudaGraphExec_t exec = nullptr;
-  static thread_local fade_model_t* exec_owner = nullptr;
-  if (exec_owner != m || !exec) {
+  if (!m->bench_exec || m->bench_coder != *coder) {
+    if (m->bench_exec) CK(cudaGraphExecDestroy(m->bench_exec));
+    m->bench_exec = nullptr;
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
     int status = compress_step(m, *coder, data_dev, L, 1, nullptr);
     cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
     if (status != FADE_OK) return status;
     CK(ce);
-    CK(cudaGraphInstantiate(&exec, graph, 0));
+    CK(cudaGraphInstantiate(&m->bench_exec, graph, 0));
     size_t n = 0;
     CK(cudaGraphGetNodes(graph, nullptr, &n));
     m->launches_per_step = (int)n;
     cudaGraphDestroy(graph);
-    exec_owner = m;
+    m->bench_coder = *coder;
   }
-  for (long long i = 0; i < steps; ++i) CK(cudaGraphLaunch(exec, m->s_main));
+  for (long long i = 0; i < steps; ++i) CK(cudaGraphLaunch(m->bench_exec, m->s_main));
   if (launches) *launches = m->launches_per_step;
   return FADE_OK;
 }

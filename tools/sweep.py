@@ -53,6 +53,7 @@ def main():
         t_roof = max(24.0 * P / (peaks["hbm_gbs"] * 1e9), 2.0 * b * 44_521_472 / (peaks["bf16_tflops"] / 2 * 1e12))
         print(json.dumps({"batch": b, "ms_per_timestep": ms, "MBps": b / ms / 1e3,
                           "roofline_MBps": b / t_roof / 1e6, "frac": t_roof * 1e3 / ms}), flush=True)
+        lib.fade_coder_destroy(coder)
         del m, mat
         torch.cuda.empty_cache()
 

@@ -20,6 +20,10 @@ namespace fade {
 
 constexpr int kWsSub = 32 * kBM * 4;        // one 128-row x 32-column fp32 box (16 KiB)
 constexpr int kWsEpiBytes = 3 * kWsSub;      // a GEGLU sub-chunk: a1, a2 and wide halves
+#ifndef FADE_WS_EPIBUFS
+#define FADE_WS_EPIBUFS 2
+#endif
+constexpr int kWsEpiBufs = FADE_WS_EPIBUFS;  // staging buffers the drain alternates
 
 template <int BN, int PAIR>
 struct WsCfg {
@@ -27,7 +31,7 @@ struct WsCfg {
   static constexpr int kABytes = kBM * kBK * 4;
   static constexpr int kBBytes = kBNL * kBK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = 2 * kWsEpiBytes;
+  static constexpr int kEpiBytes = kWsEpiBufs * kWsEpiBytes;
   static constexpr int kBarBytes = 256;
   static constexpr int kFree = kSmemLimit - 1024 - kBarBytes - kEpiBytes;
   static constexpr int kStages = (kFree / kStageBytes) > 8 ? 8 : (kFree / kStageBytes);
@@ -247,9 +251,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
       const bool geglu = P.epi == EPI_GEGLU;
       const int nsub = geglu ? BN / 64 : BN / 32;
       for (int q = 0; q < nsub; ++q, ++chunk) {
-        uint8_t* eb = epi_smem + (chunk & 1u) * kWsEpiBytes;
+        uint8_t* eb = epi_smem + (chunk % kWsEpiBufs) * kWsEpiBytes;
         // the TMA store that last read this buffer (two chunks ago) is done
-        if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (lead) {
+          if (kWsEpiBufs == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
         epi_bar();
         if (geglu) {
           // 128-column interleave block jb = [a1 | a2]; this sub-chunk is its

@@ -76,6 +76,25 @@ def test_serial_equals_pipelined_and_losses_replay():
     assert losses == b.losses            # bit-identical float trajectory on both sides
 
 
+@pytest.mark.parametrize("batch", [1, 200, 640])
+def test_default_dims_at_ragged_stream_counts(batch):
+    """Default model dims at stream counts that leave partial 128-row GEMM
+    tiles (200, 640) or a single stream: lossless, and the decoder replays the
+    encoder's losses bit for bit."""
+    from paper_2604_07239_b200 import ModelConfig, corpus
+    from paper_2604_07239_b200.pipeline import run_parallel_decompress, run_pipelined_compress
+    data = corpus.make_text(batch * 40 if batch > 1 else 300, 9)
+    res = run_pipelined_compress(data, ModelConfig(batch=batch, workers=1, seed=5))
+    assert res.losses and all(np.isfinite(res.losses))
+    lengths = np.array([len(s) for s in res.streams], dtype=np.int64)
+    offsets = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+    payload = np.frombuffer(b"".join(res.streams), np.uint8)
+    out, losses = run_parallel_decompress(payload, offsets, lengths, res.cfg, len(data),
+                                          want_losses=True)
+    assert out == data
+    assert losses == res.losses
+
+
 def test_corrupt_payload_raises():
     from paper_2604_07239_b200 import CorruptionError, corpus
     from paper_2604_07239_b200.pipeline import run_parallel_decompress, run_serial_compress

@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <array>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -619,12 +620,13 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   // WROUTE 8.  Measured (us/step): W12 after dz2 and W_f/W_head after
   // coarse_bwd (W12 runs first) 373.6; the earliest forks (2,3,7,9) 384.5;
   // W_f first (2,2 / 3,2) 382-386; W12 or W_f after bmm_bwd or later 382-429.
-  static int at[4] = {4, 3, 7, 9};
-  static bool init = false;
-  if (!init) {
-    if (const char* e = getenv("FADE_SCHED")) sscanf(e, "%d,%d,%d,%d", &at[0], &at[1], &at[2], &at[3]);
-    init = true;
-  }
+  // (a function-local static initialised once, thread-safely: models may run
+  // their steps on several host threads)
+  static const std::array<int, 4> at = [] {
+    std::array<int, 4> a{4, 3, 7, 9};
+    if (const char* e = getenv("FADE_SCHED")) sscanf(e, "%d,%d,%d,%d", &a[0], &a[1], &a[2], &a[3]);
+    return a;
+  }();
   const int ids[4] = {G_WF, G_W12, G_WUP_WCGATE, G_WROUTE_WMEM};
   int pos = 0;
   auto sides = [&]() -> int {

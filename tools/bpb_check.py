@@ -16,9 +16,10 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--extra", default="")
+    ap.add_argument("--only-extra", action="store_true", help="skip the 1 MiB reference case")
     a = ap.parse_args()
     from paper_2604_07239_b200 import ModelConfig, container, corpus
-    cases = [(1 << 20, 12, "text", 233320)]
+    cases = [] if a.only_extra else [(1 << 20, 12, "text", 233320)]
     for spec in filter(None, a.extra.split(",")):
         n, seed, kind = spec.split(":")
         cases.append((int(n), int(seed), kind, None))
@@ -32,6 +33,7 @@ def main():
         back = container.decompress_bytes(blob)
         td = time.perf_counter() - t0
         line = {"workload": f"make_{kind}({n}, {seed}), ModelConfig(seed=5)", "bytes": len(blob),
+                "compress_MBps": n / tc / 1e6, "decompress_MBps": n / td / 1e6,
                 "bits_per_byte": 8.0 * len(blob) / n, "lossless": back == data,
                 "compress_s": tc, "decompress_s": td, "mean_loss_nats": sum(res.losses) / len(res.losses)}
         if ref:

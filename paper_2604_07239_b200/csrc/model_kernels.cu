@@ -795,30 +795,121 @@ void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s) {
 // mode bit 0: input gradient dzd (reads W_U once -- the model stream's part);
 // mode bit 1: W_U gradient + Adam (the 24 B/param RMW -- run on the side
 // stream after the input gradient has read the old W_U)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
+// smem of the bulk-copy fast path: du [128], zd [32], barrier (< 1 KB), then
+// the p/m/v tiles at byte 1024
+constexpr int kBmmTileBytes = kBmmRows * 128 * 4;     // 32 rows x X = 128 floats
+constexpr int kBmmFastSmem = 1024 + 3 * kBmmTileBytes;
+
 __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_only, int mode) {
-  pdl_enter();
   const int X = M.d.X, b = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   extern __shared__ float sm[];
   float* dus = sm;          // [X]
   float* zds = sm + X;      // [X]
+  const int i0 = blockIdx.y * kBmmRows, i1 = min(X, i0 + kBmmRows);
+  const long long base = (long long)b * X * X;
+  const bool do_dx = mode & 1, do_upd = mode & 2;
+  if (X == 128 && do_upd && !grad_only) {
+    // default geometry, training path: this CTA's 32 rows of W_U p, m, v are
+    // three contiguous 16 KB blocks, pulled into smem by bulk copies issued
+    // BEFORE the dependency wait (no kernel of this step writes W_U before
+    // us; the previous step's update finished at the graph boundary), so the
+    // HBM reads overlap the tail of the du GEMM; updated in place, written
+    // back by bulk copies
+    // two halves of 16 rows, each with its own barrier: half 0 is updated
+    // and streamed back while half 1 is still landing
+    uint64_t* bar = (uint64_t*)(sm + X + kBmmRows);     // [2], after du [X] and zd [kBmmRows]
+    float* tile = (float*)((char*)sm + 1024);           // [3][32 rows][X]: p, m, v
+    constexpr int kHalf = kBmmRows / 2;
+    const int nrows = i1 - i0;
+    auto rows_of = [&](int h) { return max(0, min(kHalf, nrows - h * kHalf)); };
+    const long long off = base + (long long)i0 * X;
+    float* const gsrc[3] = {M.w[P_W_MIX].p + off, M.w[P_W_MIX].m + off, M.w[P_W_MIX].v + off};
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t bytes = (uint32_t)rows_of(h) * X * 4;
+        if (!bytes) continue;
+        mbar_expect_tx(&bar[h], 3 * bytes);
+        for (int t = 0; t < 3; ++t)
+          bulk_load(tile + t * kBmmRows * X + h * kHalf * X, gsrc[t] + h * kHalf * X, bytes, &bar[h]);
+      }
+    }
+    pdl_enter();
+    for (int i = threadIdx.x; i < X; i += blockDim.x)
+      dus[i] = sk_sum(M.sk[S_DU], (long long)M.d.B * X, (long long)b * X + i);
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) zds[i - i0] = M.a.zd[(long long)b * X + i];
+    __syncthreads();
+    const AdamScalars a = M.st->adam;
+    const float4 du4 = *(const float4*)(dus + 4 * lane);
+    constexpr int kWarps = kBmmThreads / 32;
+    float4* tp = (float4*)tile;
+    float4* tm = (float4*)(tile + kBmmRows * X);
+    float4* tv = (float4*)(tile + 2 * kBmmRows * X);
+    for (int h = 0; h < 2; ++h) {
+      const int nr = rows_of(h);
+      if (!nr) break;
+      mbar_wait(&bar[h], 0);
+      for (int r = h * kHalf + w; r < h * kHalf + nr; r += kWarps) {
+        const int q = r * 32 + lane;
+        float4 p = tp[q], mm = tm[q], v = tv[q];
+        const float acc = du4.x * p.x + du4.y * p.y + du4.z * p.z + du4.w * p.w;
+        const float zi = zds[r];
+        adam_update(a, zi * du4.x, &p.x, &mm.x, &v.x);
+        adam_update(a, zi * du4.y, &p.y, &mm.y, &v.y);
+        adam_update(a, zi * du4.z, &p.z, &mm.z, &v.z);
+        adam_update(a, zi * du4.w, &p.w, &mm.w, &v.w);
+        tp[q] = p;
+        tm[q] = mm;
+        tv[q] = v;
+        if (do_dx) {
+          const float s = warp_sum(acc);
+          if (lane == 0) M.a.dzd[(long long)b * X + i0 + r] = s;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)nr * X * 4;
+        for (int t = 0; t < 3; ++t)
+          bulk_store(gsrc[t] + h * kHalf * X, tile + t * kBmmRows * X + h * kHalf * X, bytes);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    return;
+  }
+  pdl_enter();
   for (int i = threadIdx.x; i < X; i += blockDim.x)
     dus[i] = sk_sum(M.sk[S_DU], (long long)M.d.B * X, (long long)b * X + i);
-  const int i0 = blockIdx.y * kBmmRows, i1 = min(X, i0 + kBmmRows);
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) zds[i - i0] = M.a.zd[(long long)b * X + i];
   __syncthreads();
-  const long long base = (long long)b * X * X;
   float4* __restrict__ Wp = (float4*)(M.w[P_W_MIX].p + base);
   float4* __restrict__ Wm = (float4*)(M.w[P_W_MIX].m + base);
   float4* __restrict__ Wv = (float4*)(M.w[P_W_MIX].v + base);
   float4* __restrict__ Wg = (float4*)(M.w[P_W_MIX].g + base);
   const AdamScalars a = M.st->adam;
   const int X4 = X / 4;      // X is a multiple of 4 (ModelConfig.device_check)
+  (void)do_dx;
   // one warp per row i; lanes cover 4 consecutive columns each (float4), so
   // the read-modify-write of p, m, v is one coalesced 512-byte pass per row.
   // A CTA owns kBmmRows rows of one stream: 4x more CTAs than streams keeps
   // the HBM-bound RMW evenly spread over the 148 SMs.
-  const bool do_dx = mode & 1, do_upd = mode & 2;
   constexpr int kWarps = kBmmThreads / 32;
   if (X4 == 32 && do_upd && !grad_only) {
     // default geometry (X = 128: one float4 per lane per row), the training
@@ -893,8 +984,13 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
 }
 
 void launch_bmm_bwd(const ModelPtrs& M, int grad_only, int mode, cudaStream_t s) {
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_bmm_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kBmmFastSmem);
+  (void)attr;
+  const bool fast = M.d.X == 128 && (mode & 2) && !grad_only;
   launch_pdl(k_bmm_bwd, dim3(M.d.B, cdiv(M.d.X, kBmmRows)), dim3(kBmmThreads),
-             sizeof(float) * (M.d.X + kBmmRows), s, M, grad_only, mode);
+             fast ? (size_t)kBmmFastSmem : sizeof(float) * (M.d.X + kBmmRows), s, M, grad_only,
+             mode);
 }
 
 // mixer LayerNorm + router mix + global-stream gelu (model.py:128-153 backward)

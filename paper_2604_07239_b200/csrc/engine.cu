@@ -231,12 +231,14 @@ static void plan_splits(ModelPtrs& M, std::initializer_list<SplitPlan> group) {
 struct Builder {
   GemmParams* G;
   int BN;
+  int weight_b;   // forward / input-gradient group: B is a parameter (GemmProblem::b_pre)
   int add(GemmDesc d) {
     if (G->nprob >= kMaxProblems) {
       set_last_error("too many GEMM problems in one group");
       return FADE_ERR_USAGE;
     }
     d.pair = G->pair;
+    d.b_pre = weight_b;
     return gemm_setup(&G->prob[G->nprob++], d, BN);
   }
 };
@@ -304,7 +306,10 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     if (Gs[id].pair != 2 && m->bn[id] == 256) Gs[id].pair = 2;   // 256-wide needs pairs here
     Gs[id].occ = 1;
   }
-  auto b = [&](int id) { return Builder{&Gs[id], m->bn[id]}; };
+  // B of every forward and input-gradient GEMM is a parameter that only a
+  // weight-update GEMM forked AFTER it (or the previous step) writes
+  static const bool early_b = !getenv("FADE_EARLYB") || atoi(getenv("FADE_EARLYB")) != 0;
+  auto b = [&](int id) { return Builder{&Gs[id], m->bn[id], early_b && id < G_WHEAD ? 1 : 0}; };
   Tensor4* w = M.w;
   // ablation variants (model.py:121-175) drop whole GEMMs; an empty launch
   // group is a no-op

@@ -128,12 +128,39 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
   if (PAIR == 2) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int first = blockIdx.x / PAIR, step = gridDim.x / PAIR;
+  // weight operand (GemmProblem::b_pre): the B halves of the first tile's
+  // first ring stages load before the dependency wait
+  auto load_b = [&](const WsTile& t, int i, int s) {
+    const GemmProblem& P = *t.P;
+    const int nb0 = t.n0 + (int)rank * BNL;
+    uint8_t* sb = smem + s * Cfg::kStageBytes + Cfg::kABytes;
+    const int k0 = (t.kt_begin + i) * kBK;
+    const uint32_t fb = PAIR == 2 ? mapa_shared(smem_u32(&full[s]), 0) : 0u;
+    auto load = [&](const CUtensorMap* map, void* dst, int c0, int c1) {
+      if (PAIR == 2) tma_load_2d_pair(map, fb, dst, c0, c1);
+      else tma_load_2d(map, &full[s], dst, c0, c1);
+    };
+    if (!P.b_mn) {
+      load(&P.tb, sb, k0, nb0);
+    } else {
+#pragma unroll
+      for (int c = 0; c < BNL / 32; ++c) load(&P.tb, sb + c * kBK * 128, nb0 + 32 * c, k0);
+    }
+  };
+  int npre = 0;
+  if (warp == 0 && lane == 0 && first < G.total_tiles) {
+    const WsTile t = ws_decode(G, first, (int)rank, PAIR, BN);
+    npre = t.P->b_pre ? min(t.nkt, S) : 0;
+    for (int i = 0; i < npre; ++i) {
+      if (leader) mbar_expect_tx(&full[i], PAIR * Cfg::kStageBytes);
+      load_b(t, i, i);
+    }
+  }
   pdl_wait();
 #ifdef FADE_PHASE_PROBE
   if (threadIdx.x == 0 && BN == 256) g_phase[1024 + blockIdx.x][0] = gtimer();
 #endif
-
-  const int first = blockIdx.x / PAIR, step = gridDim.x / PAIR;
 
   if (warp == 0) {
     // ---------------- TMA producer: the stage ring runs across tiles ----------------
@@ -142,14 +169,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
       for (int tile = first; tile < G.total_tiles; tile += step) {
         const WsTile t = ws_decode(G, tile, (int)rank, PAIR, BN);
         const GemmProblem& P = *t.P;
-        const int nb0 = t.n0 + (int)rank * BNL;
         for (int i = 0; i < t.nkt; ++i, ++it) {
           const int s = (int)(it % S);
-          mbar_wait(&empty[s], ((it / S) & 1u) ^ 1u);
+          const bool pre = it < (uint32_t)npre;   // B half and byte count already issued
+          if (!pre) mbar_wait(&empty[s], ((it / S) & 1u) ^ 1u);
           uint8_t* sa = smem + s * Cfg::kStageBytes;
-          uint8_t* sb = sa + Cfg::kABytes;
           const int k0 = (t.kt_begin + i) * kBK;
-          if (leader) mbar_expect_tx(&full[s], PAIR * Cfg::kStageBytes);
+          if (leader && !pre) mbar_expect_tx(&full[s], PAIR * Cfg::kStageBytes);
           const uint32_t fb = PAIR == 2 ? mapa_shared(smem_u32(&full[s]), 0) : 0u;
           auto load = [&](const CUtensorMap* map, void* dst, int c0, int c1) {
             if (PAIR == 2) tma_load_2d_pair(map, fb, dst, c0, c1);
@@ -161,12 +187,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
 #pragma unroll
             for (int c = 0; c < kBM / 32; ++c) load(&P.ta, sa + c * kBK * 128, t.m0 + 32 * c, k0);
           }
-          if (!P.b_mn) {
-            load(&P.tb, sb, k0, nb0);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BNL / 32; ++c) load(&P.tb, sb + c * kBK * 128, nb0 + 32 * c, k0);
-          }
+          if (!pre) load_b(t, i, s);
         }
       }
       if (PAIR == 2) {

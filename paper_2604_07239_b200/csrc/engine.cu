@@ -278,14 +278,17 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     m->bn[id] = 128;
     Gs[id].occ = 2;
   }
-  // the backward's narrow input-gradient GEMMs at half the shared memory
-  // (4-stage ring, ~97 KB instead of 8 stages, ~193 KB): they fit on an SM
-  // beside one weight-update CTA instead of waiting for a whole SM (-5.5 us
-  // per step together; du alone +7 us, the forward's narrow GEMMs +3 us)
+  // the backward's narrow GEMMs at half the shared memory (4-stage ring,
+  // ~97 KB instead of 8 stages / ~193 KB, or 5 stages + 3 dedicated Adam
+  // tiles for W_up): each fits on an SM beside one weight-update CTA instead
+  // of waiting for a whole SM.  Input gradients dh, du, dz, dx_r: -5.5 us per
+  // step together (du alone +7 us; the forward's narrow GEMMs +3 us); the
+  // W_up/W_cgate/W_down update (streamed Adam epilogue then): -4.5 us
   static const long occ2_ids = getenv("FADE_OCC2") ? atol(getenv("FADE_OCC2"))
                                                    : (1L << G_DH) | (1L << G_DU_DHMC) |
-                                                     (1L << G_DZ) | (1L << G_DXR_DBLOCK);
-  for (int id = 0; id < G_WHEAD; ++id)
+                                                     (1L << G_DZ) | (1L << G_DXR_DBLOCK) |
+                                                     (1L << G_WUP_WCGATE);
+  for (int id = 0; id < G_COUNT; ++id)
     if (((occ2_ids >> id) & 1) && m->bn[id] == 64) Gs[id].occ = 2;
   // W_route/W_mem update at 64-wide tiles: 288 CTAs fill both per-SM slots
   // (23 -> 16 us alone, -3 us per step); W_f measured slower that way

@@ -1280,7 +1280,9 @@ constexpr int kColAcc = 8;
 // Extra CTAs past the column blocks apply the embedding update from the
 // fixed-point accumulator (and clear it for the next step).  Last kernel of a
 // step: with `advance` it moves the step state to the next column.
-__global__ void __launch_bounds__(32 * kColWarps) k_small_adam(ModelPtrs M, int grad_only,
+// (40 registers: 512 x 40 fits on an SM beside the two W_route/W_mem update
+// CTAs still running at the end of the step; at 64 it waited for them, +1 us)
+__global__ void __maxnreg__(40) k_small_adam(ModelPtrs M, int grad_only,
                                                                double* losses, double* alpha_tape,
                                                                int col_blocks, int advance) {
   pdl_enter();

@@ -11,7 +11,8 @@ namespace fade {
 
 constexpr int kRowMax = 512;
 constexpr int kBmmThreads = 128;
-constexpr int kBmmRows = 32;      // W_U rows per k_bmm_bwd CTA
+constexpr int kBmmRows = 16;      // W_U rows per k_bmm_bwd CTA (its 25 KB of smem fits beside
+                                   // the two W_f update CTAs that share the SMs at that time)
 // The trunk kernels run 256 threads x 2 elements at <= 64 registers so four
 // CTAs fit per SM: all B = 512 rows are resident in ONE wave (512-thread CTAs
 // at 64 registers fit two per SM -> two serial waves of a latency-bound row).
@@ -810,7 +811,7 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
 
 // smem of the bulk-copy fast path: du [128], zd [32], barrier (< 1 KB), then
 // the p/m/v tiles at byte 1024
-constexpr int kBmmTileBytes = kBmmRows * 128 * 4;     // 32 rows x X = 128 floats
+constexpr int kBmmTileBytes = kBmmRows * 128 * 4;     // kBmmRows rows x X = 128 floats
 constexpr int kBmmFastSmem = 1024 + 3 * kBmmTileBytes;
 
 __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_only, int mode) {
@@ -823,16 +824,16 @@ __global__ void __launch_bounds__(kBmmThreads) k_bmm_bwd(ModelPtrs M, int grad_o
   const long long base = (long long)b * X * X;
   const bool do_dx = mode & 1, do_upd = mode & 2;
   if (X == 128 && do_upd && !grad_only) {
-    // default geometry, training path: this CTA's 32 rows of W_U p, m, v are
-    // three contiguous 16 KB blocks, pulled into smem by bulk copies issued
+    // default geometry, training path: this CTA's kBmmRows rows of W_U p, m, v
+    // are three contiguous blocks, pulled into smem by bulk copies issued
     // BEFORE the dependency wait (no kernel of this step writes W_U before
     // us; the previous step's update finished at the graph boundary), so the
     // HBM reads overlap the tail of the du GEMM; updated in place, written
     // back by bulk copies
-    // two halves of 16 rows, each with its own barrier: half 0 is updated
-    // and streamed back while half 1 is still landing
+    // two halves, each with its own barrier: half 0 is updated and streamed
+    // back while half 1 is still landing
     uint64_t* bar = (uint64_t*)(sm + X + kBmmRows);     // [2], after du [X] and zd [kBmmRows]
-    float* tile = (float*)((char*)sm + 1024);           // [3][32 rows][X]: p, m, v
+    float* tile = (float*)((char*)sm + 1024);           // [3][kBmmRows][X]: p, m, v
     constexpr int kHalf = kBmmRows / 2;
     const int nrows = i1 - i0;
     auto rows_of = [&](int h) { return max(0, min(kHalf, nrows - h * kHalf)); };

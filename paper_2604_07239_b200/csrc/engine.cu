@@ -1094,6 +1094,13 @@ int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes) {
   return FADE_OK;
 }
 
+// pipelined compression quantises on the coder stream (k_head_quant) instead
+// of in the head kernel; FADE_QUANT_CODER=0 keeps it in the head
+static bool quant_on_coder() {
+  static const bool on = !getenv("FADE_QUANT_CODER") || atoi(getenv("FADE_QUANT_CODER")) != 0;
+  return on;
+}
+
 // one compression timestep; captured once into a CUDA graph and replayed
 static int compress_step(fade_model_t* m, fade_coder_t* c, const uint8_t* data, long long L,
                          int pipelined, double* losses, double* alpha_tape = nullptr) {
@@ -1107,12 +1114,14 @@ static int compress_step(fade_model_t* m, fade_coder_t* c, const uint8_t* data, 
   io.head.ld_tgt = L;
   io.head.tgt_use_col = 1;
   io.head.adam_prep = 1;
+  io.head.skip_quant = pipelined && quant_on_coder();
   TRY(forward(m, io, true));
   if (pipelined) {
-    // CSPP: the coder stream drains this step's table while the model
-    // stream runs the backward (pipeline.py:251-287)
+    // CSPP: the coder stream quantises and drains this step's table while
+    // the model stream runs the backward (pipeline.py:251-287)
     CK(cudaEventRecord(m->ev_cum[0], m->s_main));
     CK(cudaStreamWaitEvent(m->s_coder, m->ev_cum[0], 0));
+    if (io.head.skip_quant) launch_head_quant(m->M, c->e.col, m->s_coder);
     launch_encode_col(c->e, m->d.B, data, L, m->M.a.cum, m->s_coder);
     CK(cudaEventRecord(m->ev_enc[0], m->s_coder));
   } else {

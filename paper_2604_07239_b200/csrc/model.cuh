@@ -142,8 +142,10 @@ struct HeadArgs {
   long long* dpos;
   unsigned long long* dcode;
   unsigned long long* drng;
+  int skip_quant;           // 1: the quantiser runs on the coder stream (k_head_quant)
 };
 void launch_head(const ModelPtrs& M, const HeadArgs& h, cudaStream_t s);
+void launch_head_quant(const ModelPtrs& M, const long long* colp, cudaStream_t s);
 void launch_out_bwd(const ModelPtrs& M, cudaStream_t s);
 void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s);
 void launch_bmm_bwd(const ModelPtrs& M, int grad_only, int mode, cudaStream_t s);

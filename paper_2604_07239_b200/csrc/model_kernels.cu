@@ -586,6 +586,26 @@ __device__ __forceinline__ double block_sum_d256(double v, double* red) {
 
 __device__ void adam_prep_dev(StepState* st, double lr, double b1, double b2, double eps);
 
+// fp64 softmax of one 256-logit row, thread i = symbol i: row max in float
+// (exact), z = logit - max in f64, p = exp(z) / sum.  The head kernel and the
+// coder-stream quantiser (k_head_quant) both use this exact sequence, so the
+// encoder's tables equal the decoder's bit for bit.
+__device__ __forceinline__ double row_softmax(float lg, float* fred, double* dred, double* zo,
+                                              double* so) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float mx = warp_max(lg);
+  if (lane == 0) fred[w] = mx;
+  __syncthreads();
+  mx = fred[0];
+  for (int k = 1; k < 8; ++k) mx = fmaxf(mx, fred[k]);
+  const double z = (double)lg - (double)mx;
+  const double e = exp(z);
+  const double s = block_sum_d256(e, dred);
+  *zo = z;
+  *so = s;
+  return e / s;
+}
+
 __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
   pdl_enter();
   __shared__ QuantSmem qs;
@@ -609,34 +629,27 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
     if (i == 0) record_error(st, col, b, 3);
     return;
   }
-  // row max in float (exact), then z = logit - max in f64
-  const int lane = i & 31, w = i >> 5;
-  float mx = warp_max(lg);
   __shared__ float fred[8];
-  if (lane == 0) fred[w] = mx;
-  __syncthreads();
-  mx = fred[0];
-  for (int k = 1; k < 8; ++k) mx = fmaxf(mx, fred[k]);
-  const double z = (double)lg - (double)mx;
-  const double e = exp(z);
-  const double s = block_sum_d256(e, dred);
-  const double p = e / s;
+  double z, s;
+  const double p = row_softmax(lg, fred, dred, &z, &s);
   if (H.want_probs) M.a.probs[(long long)b * kAlphabet + i] = p;
-  bool qbad;
-  const int f = quantize_sym(p, qs, &qbad);
-  if (qbad) {
-    if (i == 0) record_error(st, col, b, 4);
-    return;
+  if (!H.skip_quant) {
+    bool qbad;
+    const int f = quantize_sym(p, qs, &qbad);
+    if (qbad) {
+      if (i == 0) record_error(st, col, b, 4);
+      return;
+    }
+    const int c = block_excl_scan256(f, wsum);
+    unsigned* cum = M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd;
+    cum[i] = (unsigned)c;
+    cum_s[i] = (unsigned)c;
+    if (i == kAlphabet - 1) {
+      cum[kAlphabet] = kTotal;
+      cum_s[kAlphabet] = kTotal;
+    }
+    __syncthreads();
   }
-  const int c = block_excl_scan256(f, wsum);
-  unsigned* cum = M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd;
-  cum[i] = (unsigned)c;
-  cum_s[i] = (unsigned)c;
-  if (i == kAlphabet - 1) {
-    cum[kAlphabet] = kTotal;
-    cum_s[kAlphabet] = kTotal;
-  }
-  __syncthreads();
   if (!H.xent) return;
   int tgt;
   if (H.decode) {
@@ -674,6 +687,44 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
 
 void launch_head(const ModelPtrs& M, const HeadArgs& h, cudaStream_t s) {
   launch_pdl(k_head, dim3(M.d.B), dim3(256), 0, s, M, h);
+}
+
+// Compression's quantiser + cumulative table on the coder stream (CSPP): the
+// head kernel (skip_quant) emits the logits and the loss gradient only, so
+// the backward starts without waiting for the quantiser; this kernel
+// recomputes the row's softmax from the logits with the head's own sequence
+// and writes the table slot of the coder's column (*colp) for k_encode_col.
+__global__ void __launch_bounds__(256) k_head_quant(ModelPtrs M, const long long* colp) {
+  pdl_enter();
+  __shared__ QuantSmem qs;
+  __shared__ double dred[8];
+  __shared__ float fred[8];
+  __shared__ int wsum[8];
+  __shared__ int bad_s;
+  const int b = blockIdx.x, i = threadIdx.x;
+  const long long col = *colp;
+  if (i == 0) bad_s = 0;
+  const float lg = M.a.logits[(long long)b * kAlphabet + i];
+  __syncthreads();
+  if (!isfinite(lg)) atomicOr(&bad_s, 1);
+  __syncthreads();
+  if (bad_s) return;      // the head kernel has recorded the divergence
+  double z, s;
+  const double p = row_softmax(lg, fred, dred, &z, &s);
+  bool qbad;
+  const int f = quantize_sym(p, qs, &qbad);
+  if (qbad) {
+    if (i == 0) record_error(M.st, col, b, 4);
+    return;
+  }
+  const int c = block_excl_scan256(f, wsum);
+  unsigned* cum = M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd;
+  cum[i] = (unsigned)c;
+  if (i == kAlphabet - 1) cum[kAlphabet] = kTotal;
+}
+
+void launch_head_quant(const ModelPtrs& M, const long long* colp, cudaStream_t s) {
+  launch_pdl(k_head_quant, dim3(M.d.B), dim3(256), 0, s, M, colp);
 }
 
 // Adam bias-correction scalars from the device step counter (optim.py:26-30);

@@ -1175,13 +1175,27 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
       rr[M.sl.w_gate + q] = xt[i] * dg[o];
       rr[M.sl.w_val + q] = xt[i] * dv[o];
     }
-    for (int i = tid; i < d.D; i += blockDim.x) {
-      float a1 = 0.f, a2 = 0.f;
-      for (int o = 0; o < d.D; ++o) {
-        a1 += dg[o] * Wg[i * d.D + o];
-        a2 += dv[o] * Wv[i * d.D + o];
+    if constexpr (DT > 0) {
+      // all 8 warps: warp w takes inputs i in [4w, 4w + 4), lane = output o
+      // (coalesced weight rows), xor-tree sums -- instead of 32 threads each
+      // walking 64 dependent loads while 7 warps wait at the barrier
+      static_assert(kTrunkThreads / 32 * 4 == DT, "dx_t split");
+      const int w = tid >> 5, o = tid & 31;
+#pragma unroll
+      for (int i = 4 * w; i < 4 * w + 4; ++i) {
+        const float a1 = warp_sum(dg[o] * Wg[i * DT + o]);
+        const float a2 = warp_sum(dv[o] * Wv[i * DT + o]);
+        if (o == 0) dxs[d.H - DT + i] += a1 + a2;
       }
-      dxs[d.H - d.D + i] += a1 + a2;
+    } else {
+      for (int i = tid; i < d.D; i += blockDim.x) {
+        float a1 = 0.f, a2 = 0.f;
+        for (int o = 0; o < d.D; ++o) {
+          a1 += dg[o] * Wg[i * d.D + o];
+          a2 += dv[o] * Wv[i * d.D + o];
+        }
+        dxs[d.H - d.D + i] += a1 + a2;
+      }
     }
     __syncthreads();
   }
@@ -1280,6 +1294,41 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   __syncthreads();
   // per-symbol LayerNorm backward over D
   const float* lg = M.w[P_LOC_LN_G].p;
+  if constexpr (DT > 0) {
+    // warp w takes positions t = w, w + 8; lane = channel e (coalesced
+    // loc_hat rows).  Per-t means by xor-tree sums; the per-channel gain and
+    // bias gradients from 8 warp partials (dconv is dead now) in a fixed order
+    const int w = tid >> 5, e = tid & 31;
+    float* p1 = dcv;
+    float* p2 = dcv + 8 * DT;
+    float q1 = 0.f, q2 = 0.f;
+#pragma unroll
+    for (int t = w; t < TT; t += 8) {
+      const float dl = dls[t * DT + e];
+      const float lh = M.a.loc_hat[rH + t * DT + e];
+      q1 += dl * lh;
+      q2 += dl;
+      const float gg = dl * lg[e];
+      const float s1 = warp_sum(gg), s2 = warp_sum(gg * lh);
+      if (e == 0) {
+        locs[2 * t] = s1 / (float)DT;
+        locs[2 * t + 1] = s2 / (float)DT;
+      }
+    }
+    p1[w * DT + e] = q1;
+    p2[w * DT + e] = q2;
+    __syncthreads();
+    if (tid < DT) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        s1 += p1[k * DT + tid];
+        s2 += p2[k * DT + tid];
+      }
+      rr[M.sl.loc_g + tid] = s1;
+      rr[M.sl.loc_b + tid] = s2;
+    }
+  } else {
   for (int e = tid; e < d.D; e += blockDim.x) {
     float s1 = 0.f, s2 = 0.f;
     for (int t = 0; t < d.T; ++t) {
@@ -1299,6 +1348,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     // stash per-t means in the tail of locs (no longer needed after dloc)
     locs[2 * t] = s1 / (float)d.D;
     locs[2 * t + 1] = s2 / (float)d.D;
+  }
   }
   }   // local stream
   __syncthreads();

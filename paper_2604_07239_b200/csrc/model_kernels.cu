@@ -45,13 +45,30 @@ __device__ __forceinline__ void ln_stats(const float* xs, int n, float* red, flo
 
 // Fixed-order reduction of S split-K partial planes at element idx: four
 // independent accumulators (slices s = k mod 4) keep the loads in flight.
+template <int kSplitBatch = 4>
 __device__ __forceinline__ float split_sum(const float* __restrict__ ws, long long plane,
                                            long long idx, int S) {
-  // (the unrolled-by-4 loop resolves a[s & 3] to registers; measured faster
-  // than a hand-split main/remainder loop)
+  // loads issued kSplitBatch planes at a time (one L2 round trip per batch),
+  // then added in plane order: the same additions in the same order as a
+  // plain `a[s & 3] += ws[s]` loop, whatever the batch (kernels capped at 32
+  // registers keep 4; the head reduces its logit slices 8 at a time)
   float a[4] = {0.f, 0.f, 0.f, 0.f};
+  if constexpr (kSplitBatch == 4) {
+    // (the unrolled-by-4 loop resolves a[s & 3] to registers; measured faster
+    // than a hand-split main/remainder loop)
 #pragma unroll 4
-  for (int s = 0; s < S; ++s) a[s & 3] += ws[s * plane + idx];
+    for (int s = 0; s < S; ++s) a[s & 3] += ws[s * plane + idx];
+    return (a[0] + a[1]) + (a[2] + a[3]);
+  }
+  for (int s0 = 0; s0 < S; s0 += kSplitBatch) {
+    float v[kSplitBatch];
+#pragma unroll
+    for (int k = 0; k < kSplitBatch; ++k)
+      if (s0 + k < S) v[k] = ws[(s0 + k) * plane + idx];
+#pragma unroll
+    for (int k = 0; k < kSplitBatch; ++k)
+      if (s0 + k < S) a[k & 3] += v[k];
+  }
   return (a[0] + a[1]) + (a[2] + a[3]);
 }
 // Row [rH, rH + n) of S split-K planes reduced into dst (smem), bit-identical
@@ -81,8 +98,9 @@ __device__ __forceinline__ void split_row(float* dst, float* part, const float* 
 }
 
 // element idx of a narrow GEMM's output [B][N] (plane = B*N), reduced over its slices
+template <int kSplitBatch = 4>
 __device__ __forceinline__ float sk_sum(const SplitBuf& k, long long plane, long long idx) {
-  return split_sum(k.ws, plane, idx, k.S);
+  return split_sum<kSplitBatch>(k.ws, plane, idx, k.S);
 }
 
 // LayerNorm backward over one row (ops.py:103-113): returns dx into dxs (smem or
@@ -618,7 +636,7 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
   StepState* st = M.st;
   const long long col = st->col;
   if (i == 0) bad_s = 0;
-  const float lg = sk_sum(M.sk[S_LOGITS], (long long)M.d.B * kAlphabet, (long long)b * kAlphabet + i);
+  const float lg = sk_sum<8>(M.sk[S_LOGITS], (long long)M.d.B * kAlphabet, (long long)b * kAlphabet + i);
   M.a.logits[(long long)b * kAlphabet + i] = lg;
   __syncthreads();
   if (!isfinite(lg)) atomicOr(&bad_s, 1);

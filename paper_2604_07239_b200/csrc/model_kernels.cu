@@ -165,14 +165,23 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   if constexpr (DT > 0) {
     // weights into smem as float4: at the compiled geometry (D = 32, H = 512)
     // every small-arena offset is a multiple of 4 floats (make_small_layout)
+    // (cp.async: no register round trip before the embedding gather; they
+    // are first read after the LayerNorm, behind a wait_all + barrier)
     const float4* g4 = (const float4*)M.w[P_W_GATE].p;
     const float4* v4 = (const float4*)M.w[P_W_VAL].p;
     const float4* k4 = (const float4*)M.w[P_CONV_K].p;
+    auto cp16 = [](float* dst, const float4* src) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(dst)),
+                   "l"(src)
+                   : "memory");
+    };
     for (int j = tid; j < d.D * d.D / 4; j += blockDim.x) {
-      ((float4*)wg)[j] = g4[j];
-      ((float4*)wv)[j] = v4[j];
+      cp16(wg + 4 * j, g4 + j);
+      cp16(wv + 4 * j, v4 + j);
     }
-    for (int j = tid; j < d.K * d.D * d.D / 4; j += blockDim.x) ((float4*)ck)[j] = k4[j];
+    for (int j = tid; j < d.K * d.D * d.D / 4; j += blockDim.x) cp16(ck + 4 * j, k4 + j);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   } else {
     for (int j = tid; j < d.D * d.D; j += blockDim.x) {
       wg[j] = M.w[P_W_GATE].p[j];
@@ -199,6 +208,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     M.a.x[rH + j] = xv;
   }
   if (tid == 0) M.a.x_inv[b] = inv;
+  if constexpr (DT > 0) asm volatile("cp.async.wait_all;" ::: "memory");   // weights (and roll reads) landed
   __syncthreads();
 
   // GeGLU block of the newest symbol: gelu(x_t W_gate) * (x_t W_val)

@@ -61,6 +61,9 @@ typedef struct {
 FADE_API const char* fade_last_error(void);
 FADE_API int fade_abi_version(void);
 FADE_API int fade_device_count(void);
+/* Compute capability and name of `device` (the per-shard fingerprint of the
+ * v2 container records which GPU architecture wrote each shard). */
+FADE_API int fade_device_arch(int device, int* major, int* minor, char* name, int name_len);
 
 /* ---- 1. kernel table: kernels.py:48-233 (device pointers) ----------------- */
 
@@ -133,26 +136,36 @@ FADE_API int fade_model_loss_grads(fade_model_t* m, const uint8_t* ctx, const ui
 /* Compress a B x L stream matrix (row b = stream b, pipeline.py:35-64).
  * `data` is host memory (on_device = 0) or device memory (on_device = 1).
  * The first `warm` columns are uniform-coded with no model call
- * (pipeline.py:193,212-213).  m may be NULL when L <= warm.
+ * (pipeline.py:193,212-213).  m may be NULL when L <= warm; the call then
+ * runs on `device` (with a model, on the model's device).  Every call leaves
+ * the calling thread's current CUDA device as it found it.
  * pipelined = 1 runs the coder on its own CUDA stream, double-buffered against
  * the model (the CSPP of pipeline.py:229-299); 0 is the serial order.  Both
- * produce identical bytes.  Outputs: lengths[B] (host), losses[L-warm] and
- * alpha[3*(L-warm)] (host, may be NULL: per-step router mean/min/max for the
- * metrics tape, pipeline.py:162-185); fetch the bytes with fade_coder_fetch. */
+ * produce identical bytes.  Outputs (host, each may be NULL): lengths[B];
+ * losses[L-warm]; alpha[3*(L-warm)] per-step router mean/min/max for the
+ * metrics tape (pipeline.py:162-185); tape[5*(L-warm)] the device event tape
+ * (%globaltimer ns per model step: table fill begins, table full, drain
+ * begins, drain done, step done -- the PingPongBuffer slot transitions of
+ * pipeline.py:86-149 as the device ran them).  Fetch the bytes with
+ * fade_coder_fetch.  A divergence reports err->step = Predictor.step_count at
+ * the failing column (model.py:190-193,208-209: column - warm for a fresh
+ * model); a coder error reports the column. */
 typedef struct fade_coder fade_coder_t;
-FADE_API int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, int64_t warm,
-                  int on_device, int pipelined, int64_t* lengths, double* losses,
-                  double* alpha, fade_coder_t** coder, fade_error_t* err);
+FADE_API int fade_compress(fade_model_t* m, int device, int batch, const uint8_t* data, int64_t L,
+                  int64_t warm, int on_device, int pipelined, int64_t* lengths, double* losses,
+                  double* alpha, uint64_t* tape, fade_coder_t** coder, fade_error_t* err);
 /* Concatenated stream bytes (payload order of container.py:99-110). */
 FADE_API int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes);
 FADE_API int fade_coder_destroy(fade_coder_t* c);
 
 /* Decompress (pipeline.py:310-396): payload host bytes, lengths[B] host.
- * Writes the B x L matrix to out (host), losses[L-warm] and alpha[3*(L-warm)]
- * (each may be NULL). */
-FADE_API int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t nbytes,
-                    const int64_t* lengths, int64_t L, int64_t warm, uint8_t* out,
-                    double* losses, double* alpha, fade_error_t* err);
+ * Writes the B x L matrix to out (host), losses[L-warm], alpha[3*(L-warm)]
+ * and tape[5*(L-warm)] (each may be NULL; tape slots 2-3 stamp the decoder
+ * inside the head kernel).  `device` as for fade_compress. */
+FADE_API int fade_decompress(fade_model_t* m, int device, int batch, const uint8_t* payload,
+                    int64_t nbytes, const int64_t* lengths, int64_t L, int64_t warm,
+                    uint8_t* out, double* losses, double* alpha, uint64_t* tape,
+                    fade_error_t* err);
 
 /* ---- measurement hooks (bench.py) ------------------------------------------ */
 

@@ -40,6 +40,7 @@ SIGNATURES = {
     "fade_last_error": (ctypes.c_char_p, []),
     "fade_abi_version": (i32, []),
     "fade_device_count": (i32, []),
+    "fade_device_arch": (i32, [i32, P(i32), P(i32), ctypes.c_char_p, i32]),
     "fade_quantize_rows": (i64, [vp, vp, i64, i64, vp]),
     "fade_encode_step": (i64, [vp, i64, vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, vp]),
     "fade_flush": (i64, [vp, vp, vp, vp, i64, vp, i64, i64, vp]),
@@ -57,10 +58,11 @@ SIGNATURES = {
     "fade_model_train_step": (i32, [vp, vp, P(f64), P(FadeError)]),
     "fade_model_forward_debug": (i32, [vp, vp, ctypes.c_char_p, vp]),
     "fade_model_loss_grads": (i32, [vp, vp, vp, P(f64)]),
-    "fade_compress": (i32, [vp, i32, vp, i64, i64, i32, i32, vp, vp, vp, P(vp), P(FadeError)]),
+    "fade_compress": (i32, [vp, i32, i32, vp, i64, i64, i32, i32, vp, vp, vp, vp, P(vp),
+                            P(FadeError)]),
     "fade_coder_fetch": (i32, [vp, vp, i64]),
     "fade_coder_destroy": (i32, [vp]),
-    "fade_decompress": (i32, [vp, i32, vp, i64, vp, i64, i64, vp, vp, vp, P(FadeError)]),
+    "fade_decompress": (i32, [vp, i32, i32, vp, i64, vp, i64, i64, vp, vp, vp, vp, P(FadeError)]),
     "fade_bench_compress_steps": (i32, [vp, vp, i64, i64, i64, P(vp), P(i32), vp]),
     "fade_model_stream": (i32, [vp, P(vp)]),
     "fade_bench_probe": (i32, [vp, i32, i32, P(f64), P(f64), P(f64)]),
@@ -95,6 +97,29 @@ def last_error() -> str:
 def check(status: int, what: str) -> None:
     if status != 0:
         raise RuntimeError(f"{what} failed (status {status}): {last_error()}")
+
+
+_BUILD_ID = None
+
+
+def build_id() -> str:
+    """First 16 hex digits of the loaded library's sha256: identifies the exact
+    kernels (and so the float trajectory) that wrote a container."""
+    global _BUILD_ID
+    if _BUILD_ID is None:
+        import hashlib
+        with open(LIB_PATH, "rb") as fh:
+            _BUILD_ID = hashlib.sha256(fh.read()).hexdigest()[:16]
+    return _BUILD_ID
+
+
+def device_arch(device: int) -> str:
+    """e.g. 'sm_100 NVIDIA B200' for the given CUDA device."""
+    ma, mi = ctypes.c_int(), ctypes.c_int()
+    name = ctypes.create_string_buffer(128)
+    check(lib().fade_device_arch(int(device), ctypes.byref(ma), ctypes.byref(mi), name, 128),
+          "fade_device_arch")
+    return f"sm_{ma.value}{mi.value} {name.value.decode()}"
 
 
 def require_device() -> None:

@@ -38,6 +38,10 @@ static int cuda_fail(cudaError_t e, const char* what) {
   return FADE_ERR_CUDA;
 }
 #define CK(expr) TRY(cuda_fail((expr), #expr))
+// the ABI call runs on this device; the caller's current device is restored
+#define ON_DEVICE(dev)          \
+  DeviceScope _dscope(dev);     \
+  CK(_dscope.status)
 
 static size_t align_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
 
@@ -67,15 +71,19 @@ using namespace fade;
 // memory for reuse: a plain cudaFree can stall for 100+ ms (it synchronises and
 // unmaps), which showed up as a variable per-call cost in compress_bytes.
 static cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t s) {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
+  static std::mutex mu;
+  static std::vector<bool> done;   // per device: release threshold raised
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)done.size() <= dev) done.resize(dev + 1, false);
     cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (!done[dev] && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t keep = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      done[dev] = true;
     }
-  });
+  }
   return cudaMallocAsync(p, bytes, s);
 }
 static void dev_free(void* p, cudaStream_t s) {
@@ -84,6 +92,7 @@ static void dev_free(void* p, cudaStream_t s) {
 
 struct fade_model {
   fade_config_t cfg;
+  long long step_offset = 0;    // column - Predictor.step_count of the running call
   Dims d;
   SmallLayout sl;
   int device = 0;
@@ -113,11 +122,18 @@ struct fade_model {
 
 struct fade_coder {
   int B = 0;
+  int device = 0;
   long long L = 0, cap = 0;
   void* mem = nullptr;
-  EncState e;
+  EncState e{};
   std::vector<long long> lengths;
   cudaStream_t s = nullptr;
+  ~fade_coder() {   // every exit path, the error paths of fade_compress included
+    if (!mem) return;
+    DeviceScope ds(device);
+    cudaFreeAsync(mem, s);
+    cudaStreamSynchronize(s);
+  }
 };
 
 namespace fade {
@@ -284,7 +300,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   // of waiting for a whole SM.  Input gradients dh, du, dz, dx_r: -5.5 us per
   // step together (du alone +7 us; the forward's narrow GEMMs +3 us); the
   // W_up/W_cgate/W_down update (streamed Adam epilogue then): -4.5 us
-  static const long occ2_ids = getenv("FADE_OCC2") ? atol(getenv("FADE_OCC2"))
+  static const long occ2_ids = knob("FADE_OCC2") ? atol(knob("FADE_OCC2"))
                                                    : (1L << G_DH) | (1L << G_DU_DHMC) |
                                                      (1L << G_DZ) | (1L << G_DXR_DBLOCK) |
                                                      (1L << G_WUP_WCGATE);
@@ -292,7 +308,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     if (((occ2_ids >> id) & 1) && m->bn[id] == 64) Gs[id].occ = 2;
   // W_route/W_mem update at 64-wide tiles: 288 CTAs fill both per-SM slots
   // (23 -> 16 us alone, -3 us per step); W_f measured slower that way
-  static const long bn64_ids = getenv("FADE_BN64") ? atol(getenv("FADE_BN64"))
+  static const long bn64_ids = knob("FADE_BN64") ? atol(knob("FADE_BN64"))
                                                    : (1L << G_WROUTE_WMEM);
   for (int id = 0; id < G_COUNT; ++id)
     if ((bn64_ids >> id) & 1) m->bn[id] = 64;
@@ -301,7 +317,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   // FNR project GEMM F (split-K 18, 144 CTAs): -1.7 us;
   // neutral or slower for the narrower W_f / W_route / W_mem updates and the
   // other forward GEMMs)
-  static const long pair_ids = getenv("FADE_PAIR") ? atol(getenv("FADE_PAIR"))
+  static const long pair_ids = knob("FADE_PAIR") ? atol(knob("FADE_PAIR"))
                                                    : (1L << G_W12) | (1L << G_DWIDE) |
                                                      (1L << G_DZ2) | (1L << G_F);
   for (int id = 0; id < G_COUNT; ++id) {
@@ -311,7 +327,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   }
   // persistent warp-specialised kernel (gemm_ws.cuh) for the store/GeGLU GEMMs
   // (the FNR expand GEMM: -2.6 us per step; neutral or slower elsewhere)
-  static const long ws_ids = getenv("FADE_WS") ? atol(getenv("FADE_WS")) : (1L << G_E12);
+  static const long ws_ids = knob("FADE_WS") ? atol(knob("FADE_WS")) : (1L << G_E12);
   for (int id = 0; id < G_COUNT; ++id) {
     if (!((ws_ids >> id) & 1)) continue;
     Gs[id].ws = 1;
@@ -320,7 +336,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   }
   // B of every forward and input-gradient GEMM is a parameter that only a
   // weight-update GEMM forked AFTER it (or the previous step) writes
-  static const bool early_b = !getenv("FADE_EARLYB") || atoi(getenv("FADE_EARLYB")) != 0;
+  static const bool early_b = !knob("FADE_EARLYB") || atoi(knob("FADE_EARLYB")) != 0;
   auto b = [&](int id) { return Builder{&Gs[id], m->bn[id], early_b && id < G_WHEAD ? 1 : 0}; };
   Tensor4* w = M.w;
   // ablation variants (model.py:121-175) drop whole GEMMs; an empty launch
@@ -443,9 +459,11 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
 // FADE_DBG_SKIP (1 side-stream, 2 model-stream GEMMs) and FADE_DBG_SKIPID (a
 // bit per GemmId) drop GEMM launches to measure what each costs on the
 // critical path.  Timing experiments only: the results are wrong.
+// (experiments build only: the shipped library never skips work)
 static int run_gemm(fade_model* m, int id, cudaStream_t s, bool grad_only = false) {
-  static const int dbg_skip = getenv("FADE_DBG_SKIP") ? atoi(getenv("FADE_DBG_SKIP")) : 0;
-  static const long dbg_ids = getenv("FADE_DBG_SKIPID") ? atol(getenv("FADE_DBG_SKIPID")) : 0;
+#ifdef FADE_EXPERIMENTS
+  static const int dbg_skip = knob("FADE_DBG_SKIP") ? atoi(knob("FADE_DBG_SKIP")) : 0;
+  static const long dbg_ids = knob("FADE_DBG_SKIPID") ? atol(knob("FADE_DBG_SKIPID")) : 0;
   static std::once_flag warned;
   if (dbg_skip || dbg_ids)
     std::call_once(warned, [] {
@@ -454,6 +472,7 @@ static int run_gemm(fade_model* m, int id, cudaStream_t s, bool grad_only = fals
   if ((dbg_skip & 1) && s == m->s_side) return FADE_OK;
   if ((dbg_skip & 2) && s != m->s_side) return FADE_OK;
   if (dbg_ids & (1L << id)) return FADE_OK;
+#endif
   return gemm_launch(grad_only ? m->Gg[id] : m->G[id], m->bn[id], s);
 }
 
@@ -468,7 +487,7 @@ static int allocate(fade_model* m) {
   const int tiles = cdiv(B, kBM) * cdiv(H, kWideBN);
   M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
   M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
-  if (const char* e = getenv("FADE_SPLITS_F")) M.splits_f = std::max(1, atoi(e));   // experiments
+  if (const char* e = knob("FADE_SPLITS_F")) M.splits_f = std::max(1, atoi(e));   // experiments
   M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
   // Only the forward's narrow GEMMs split: in the backward the side stream's
   // weight updates hold most SMs, and a 128-CTA input-gradient GEMM waits for
@@ -477,7 +496,7 @@ static int allocate(fade_model* m) {
   for (int k = 0; k < S_COUNT; ++k) M.sk[k].S = 1;
   // the router GEMM (K = H) shares a launch with the split-K W_mem GEMM
   // (K = C / 16 per slice): two slices balance the two
-  static const int rsplit = getenv("FADE_RPRE_SPLIT") ? atoi(getenv("FADE_RPRE_SPLIT")) : 2;
+  static const int rsplit = knob("FADE_RPRE_SPLIT") ? atoi(knob("FADE_RPRE_SPLIT")) : 2;
   M.sk[S_RPRE].S = std::max(1, rsplit);
   plan_splits(M, {{S_ZD, B, X, H}});
   plan_splits(M, {{S_INNER, B, H, X}, {S_CPRE, B, H, H}});
@@ -574,7 +593,7 @@ struct StepIO {
 // carve-out: -3 us per step.  Pinning p and m (67 MB) measured +32 us (the
 // carve-out starves the other kernels' L2).  FADE_L2PIN=0/1/2 overrides.
 static int l2_pin_mode() {
-  static const int mode = getenv("FADE_L2PIN") ? atoi(getenv("FADE_L2PIN")) : 1;
+  static const int mode = knob("FADE_L2PIN") ? atoi(knob("FADE_L2PIN")) : 1;
   return mode;
 }
 struct L2Pin {
@@ -641,7 +660,7 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   // their steps on several host threads)
   static const std::array<int, 4> at = [] {
     std::array<int, 4> a{4, 3, 7, 9};
-    if (const char* e = getenv("FADE_SCHED")) sscanf(e, "%d,%d,%d,%d", &a[0], &a[1], &a[2], &a[3]);
+    if (const char* e = knob("FADE_SCHED")) sscanf(e, "%d,%d,%d,%d", &a[0], &a[1], &a[2], &a[3]);
     return a;
   }();
   const int ids[4] = {G_WF, G_W12, G_WUP_WCGATE, G_WROUTE_WMEM};
@@ -715,7 +734,11 @@ static int check_error(fade_model* m, fade_error_t* err) {
     err->kind = kind;
     err->why = why;
     err->stream = stream;
-    err->step = code == 6 ? -1 : step;
+    // errors are keyed by column so the earliest one in time wins; a coder
+    // error reports the column (coder.py:85-86,117-128), a divergence the
+    // model's step_count at that column (model.py:190-193,208-209), which in
+    // the executors is column - warm
+    err->step = code == 6 ? -1 : (kind == FADE_ERR_DIVERGED ? step - m->step_offset : step);
   }
   set_last_error(msg);
   // reset so the model object stays usable after the caller handles the error
@@ -724,11 +747,50 @@ static int check_error(fade_model* m, fade_error_t* err) {
   return kind;
 }
 
+// position the device step state at column `col`; losses[0] is the loss of
+// column loss_base.  step_count (Predictor.step_count) is unchanged, so the
+// divergence report maps a column back to it through step_offset.
 static int set_col(fade_model* m, long long col, long long loss_base) {
-  long long v[2] = {col, 0};
-  CK(cudaMemcpyAsync(&m->st->col, &col, sizeof(long long), cudaMemcpyHostToDevice, m->s_main));
-  v[1] = loss_base;
+  long long v[2] = {col, loss_base}, sc = 0;
+  CK(cudaMemcpyAsync(&m->st->col, &v[0], sizeof(long long), cudaMemcpyHostToDevice, m->s_main));
   CK(cudaMemcpyAsync(&m->st->loss_base, &v[1], sizeof(long long), cudaMemcpyHostToDevice, m->s_main));
+  CK(cudaMemcpyAsync(&sc, &m->st->step_count, sizeof(long long), cudaMemcpyDeviceToHost, m->s_main));
+  CK(cudaStreamSynchronize(m->s_main));
+  m->step_offset = col - sc;
+  return FADE_OK;
+}
+
+// runs a callable when the scope exits (every error path included)
+template <class F>
+struct Defer {
+  F f;
+  ~Defer() { f(); }
+};
+template <class F>
+static Defer<F> defer(F f) {
+  return Defer<F>{f};
+}
+
+// Captures `body` (one timestep on the model stream) into a graph and replays
+// it `n` times.  The event tape pointer rides in the captured kernel
+// parameters only.
+template <class Body>
+static int replay_steps(fade_model_t* m, long long n, unsigned long long* tape, Body body) {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  auto cleanup = defer([&] {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  });
+  m->M.tape = tape;
+  CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
+  const int status = body();
+  const cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
+  m->M.tape = nullptr;
+  if (status != FADE_OK) return status;
+  CK(ce);
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  for (long long i = 0; i < n; ++i) CK(cudaGraphLaunch(exec, m->s_main));
   CK(cudaStreamSynchronize(m->s_main));
   return FADE_OK;
 }
@@ -765,12 +827,12 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   d.Ep = (cfg->expand_dim + 63) / 64 * 64;
   d.K = cfg->conv_kernel;
   m->sl = make_small_layout(d);
-  CK(cudaSetDevice(device));
+  ON_DEVICE(device);
   // the model stream is the critical path: its CTAs take SM slots ahead of
   // the side stream's (HBM-bound) weight-update GEMMs when both are pending
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  static const int dbg_prio = getenv("FADE_DBG_PRIO") ? atoi(getenv("FADE_DBG_PRIO")) : 1;
+  static const int dbg_prio = knob("FADE_DBG_PRIO") ? atoi(knob("FADE_DBG_PRIO")) : 1;
   if (!dbg_prio) prio_hi = prio_lo;
   CK(cudaStreamCreateWithPriority(&m->s_main, cudaStreamNonBlocking, prio_hi));
   CK(cudaStreamCreateWithPriority(&m->s_side, cudaStreamNonBlocking, prio_lo));
@@ -800,7 +862,7 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
 
 int fade_model_destroy(fade_model_t* m) {
   if (!m) return FADE_OK;
-  cudaSetDevice(m->device);
+  DeviceScope dscope(m->device);
   cudaDeviceSynchronize();
   if (m->bench_exec) cudaGraphExecDestroy(m->bench_exec);
   dev_free(m->mem, m->s_main);
@@ -852,7 +914,7 @@ int fade_model_set_tensor(fade_model_t* m, int kind, int index, const float* hos
     set_last_error("set_tensor: bad kind/index/size");
     return FADE_ERR_USAGE;
   }
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   float* dev = tensor_base(m, kind, index);
   if (index == P_W_E1 || index == P_W_E2)
     return copy_w12(m, dev, index == P_W_E2, const_cast<float*>(host), true);
@@ -865,7 +927,7 @@ int fade_model_get_tensor(fade_model_t* m, int kind, int index, float* host, int
     set_last_error("get_tensor: bad kind/index/size");
     return FADE_ERR_USAGE;
   }
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   CK(cudaDeviceSynchronize());
   float* dev = tensor_base(m, kind, index);
   if (index == P_W_E1 || index == P_W_E2) return copy_w12(m, dev, index == P_W_E2, host, false);
@@ -874,20 +936,20 @@ int fade_model_get_tensor(fade_model_t* m, int kind, int index, float* host, int
 }
 
 int fade_model_set_cache(fade_model_t* m, const float* host) {
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   CK(cudaMemcpy(m->M.a.cache, host, sizeof(float) * m->d.B * m->d.C, cudaMemcpyHostToDevice));
   return FADE_OK;
 }
 
 int fade_model_get_cache(fade_model_t* m, float* host) {
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(host, m->M.a.cache, sizeof(float) * m->d.B * m->d.C, cudaMemcpyDeviceToHost));
   return FADE_OK;
 }
 
 int fade_model_set_counters(fade_model_t* m, int64_t adam_t, int64_t step_count) {
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   long long v[2] = {adam_t, step_count};
   CK(cudaMemcpy(&m->st->adam_t, &v[0], sizeof(long long), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(&m->st->step_count, &v[1], sizeof(long long), cudaMemcpyHostToDevice));
@@ -895,7 +957,7 @@ int fade_model_set_counters(fade_model_t* m, int64_t adam_t, int64_t step_count)
 }
 
 int fade_model_get_counters(fade_model_t* m, int64_t* adam_t, int64_t* step_count) {
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   CK(cudaDeviceSynchronize());
   long long v[2];
   CK(cudaMemcpy(&v[0], &m->st->adam_t, sizeof(long long), cudaMemcpyDeviceToHost));
@@ -915,17 +977,25 @@ static StepIO api_io(fade_model_t* m) {
 
 int fade_model_predict(fade_model_t* m, const uint8_t* ctx, double* probs, double* alpha,
                        fade_error_t* err) {
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   const Dims& d = m->d;
   int64_t sc = 0, t = 0;
   TRY(fade_model_get_counters(m, &t, &sc));
   TRY(set_col(m, sc, sc));
+  // the trunk kernel rolls the cache in place before the head can find a
+  // non-finite logit; the reference commits the cache only after its finite
+  // check (model.py:190-196), so a failed predict restores the snapshot
+  const size_t cbytes = sizeof(float) * d.B * d.C;
+  CK(cudaMemcpyAsync(m->cache_snap, m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
   CK(cudaMemcpyAsync(m->ctx_buf, ctx, (size_t)d.B * d.T, cudaMemcpyHostToDevice, m->s_main));
   StepIO io = api_io(m);
   io.head.want_probs = 1;
   TRY(forward(m, io, true));
   CK(cudaStreamSynchronize(m->s_main));
-  TRY(check_error(m, err));
+  if (int st = check_error(m, err)) {
+    CK(cudaMemcpy(m->M.a.cache, m->cache_snap, cbytes, cudaMemcpyDeviceToDevice));
+    return st;
+  }
   if (probs)
     CK(cudaMemcpy(probs, m->M.a.probs, sizeof(double) * d.B * 256, cudaMemcpyDeviceToHost));
   if (alpha) {
@@ -950,7 +1020,7 @@ int fade_model_train_step(fade_model_t* m, const uint8_t* targets, double* loss,
     set_last_error("train_step requires a preceding predict");
     return FADE_ERR_STATE;
   }
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   const Dims& d = m->d;
   CK(cudaMemcpyAsync(m->tgt_buf, targets, (size_t)d.B, cudaMemcpyHostToDevice, m->s_main));
   StepIO io = api_io(m);
@@ -984,7 +1054,7 @@ static const float* part_ptr(fade_model_t* m, const char* part, int* width) {
 }
 
 int fade_model_forward_debug(fade_model_t* m, const uint8_t* ctx, const char* part, float* out) {
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   int width = 0;
   const float* src = part_ptr(m, part, &width);
   if (!src) {
@@ -1005,7 +1075,7 @@ int fade_model_forward_debug(fade_model_t* m, const uint8_t* ctx, const char* pa
 }
 
 int fade_model_loss_grads(fade_model_t* m, const uint8_t* ctx, const uint8_t* targets, double* loss) {
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   const Dims& d = m->d;
   const size_t cbytes = sizeof(float) * d.B * d.C;
   CK(cudaMemcpyAsync(m->cache_snap, m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
@@ -1030,10 +1100,11 @@ int fade_model_loss_grads(fade_model_t* m, const uint8_t* ctx, const uint8_t* ta
 // ---------------------------------------------------------------------------
 // executors
 
-static int coder_create(int B, long long L, cudaStream_t s, fade_coder_t** out) {
+static int coder_create(int B, long long L, int device, cudaStream_t s, fade_coder_t** out) {
   std::unique_ptr<fade_coder> c(new fade_coder());
   c->B = B;
   c->L = L;
+  c->device = device;
   c->cap = 2 * L + 16;       // <= 2 bytes per symbol + the 5-shift flush
   c->s = s;
   const size_t nB = (size_t)B;
@@ -1062,14 +1133,12 @@ static int coder_create(int B, long long L, cudaStream_t s, fade_coder_t** out) 
 }
 
 int fade_coder_destroy(fade_coder_t* c) {
-  if (!c) return FADE_OK;
-  dev_free(c->mem, c->s);
-  cudaStreamSynchronize(c->s);
-  delete c;
+  delete c;   // frees its device buffers on its own device
   return FADE_OK;
 }
 
 int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes) {
+  ON_DEVICE(c->device);
   long long total = 0;
   std::vector<long long> off(c->B);
   for (int b = 0; b < c->B; ++b) {
@@ -1083,13 +1152,16 @@ int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes) {
   if (total == 0) return FADE_OK;
   long long* doff = nullptr;
   uint8_t* dout = nullptr;
+  auto cleanup = defer([&] {
+    dev_free(doff, c->s);
+    dev_free(dout, c->s);
+    cudaStreamSynchronize(c->s);
+  });
   CK(dev_alloc((void**)&doff, sizeof(long long) * c->B, c->s));
   CK(dev_alloc((void**)&dout, (size_t)total, c->s));
   CK(cudaMemcpyAsync(doff, off.data(), sizeof(long long) * c->B, cudaMemcpyHostToDevice, c->s));
   launch_compact(c->e, c->B, doff, dout, c->s);
   CK(cudaMemcpyAsync(payload, dout, (size_t)total, cudaMemcpyDeviceToHost, c->s));
-  dev_free(doff, c->s);
-  dev_free(dout, c->s);
   CK(cudaStreamSynchronize(c->s));
   return FADE_OK;
 }
@@ -1097,7 +1169,7 @@ int fade_coder_fetch(fade_coder_t* c, uint8_t* payload, int64_t nbytes) {
 // pipelined compression quantises on the coder stream (k_head_quant) instead
 // of in the head kernel; FADE_QUANT_CODER=0 keeps it in the head
 static bool quant_on_coder() {
-  static const bool on = !getenv("FADE_QUANT_CODER") || atoi(getenv("FADE_QUANT_CODER")) != 0;
+  static const bool on = !knob("FADE_QUANT_CODER") || atoi(knob("FADE_QUANT_CODER")) != 0;
   return on;
 }
 
@@ -1133,9 +1205,9 @@ static int compress_step(fade_model_t* m, fade_coder_t* c, const uint8_t* data, 
   return FADE_OK;
 }
 
-int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, int64_t warm,
-                  int on_device, int pipelined, int64_t* lengths, double* losses, double* alpha,
-                  fade_coder_t** coder_out, fade_error_t* err) {
+int fade_compress(fade_model_t* m, int device, int batch, const uint8_t* data, int64_t L,
+                  int64_t warm, int on_device, int pipelined, int64_t* lengths, double* losses,
+                  double* alpha, uint64_t* tape, fade_coder_t** coder_out, fade_error_t* err) {
   *coder_out = nullptr;
   if (m && m->d.B != batch) {
     set_last_error("compress: batch does not match the model");
@@ -1145,9 +1217,10 @@ int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, in
     set_last_error("compress: a model is required when L > warm");
     return FADE_ERR_USAGE;
   }
+  const int dev = m ? m->device : device;
+  ON_DEVICE(dev);
   cudaStream_t s = m ? m->s_main : nullptr;
-  if (m) CK(cudaSetDevice(m->device));
-  static const bool timing = getenv("FADE_TIMING") != nullptr;
+  static const bool timing = getenv("FADE_TIMING") != nullptr;   // host timestamps only
   auto now = [] { return std::chrono::steady_clock::now(); };
   const auto tA = now();
   auto stamp = [&](const char* what) {
@@ -1158,7 +1231,18 @@ int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, in
     }
   };
   const size_t nbytes = (size_t)batch * (size_t)L;
+  const long long nsteps = L > warm ? L - warm : 0;
   uint8_t* dmat = nullptr;
+  double* dloss = nullptr;
+  double* dalpha = nullptr;
+  unsigned long long* dtape = nullptr;
+  auto cleanup = defer([&] {
+    dev_free(dmat, s);
+    dev_free(dloss, s);
+    dev_free(dalpha, s);
+    dev_free(dtape, s);
+    cudaStreamSynchronize(s);
+  });
   const uint8_t* mat = data;
   if (!on_device && nbytes) {
     CK(dev_alloc((void**)&dmat, nbytes, s));
@@ -1167,68 +1251,48 @@ int fade_compress(fade_model_t* m, int batch, const uint8_t* data, int64_t L, in
   }
   stamp("upload");
   fade_coder_t* c = nullptr;
-  TRY(coder_create(batch, L, s, &c));
+  TRY(coder_create(batch, L, dev, s, &c));
   std::unique_ptr<fade_coder> guard(c);
   launch_encode_warm(c->e, batch, mat, L, warm, s);
   stamp("coder");
-  double* dloss = nullptr;
-  int status = FADE_OK;
-  if (m && L > warm) {
+  if (m && nsteps > 0) {
     TRY(set_col(m, warm, warm));
-    CK(dev_alloc((void**)&dloss, sizeof(double) * (size_t)(L - warm), m->s_main));
-    double* dalpha = nullptr;
-    if (alpha) CK(dev_alloc((void**)&dalpha, sizeof(double) * 3 * (size_t)(L - warm), m->s_main));
-    // capture one timestep into a graph, replay it L - warm times
-    cudaGraph_t graph;
-    cudaGraphExec_t exec;
-    CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
-    status = compress_step(m, c, mat, L, pipelined, dloss, dalpha);
-    cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
-    if (status != FADE_OK) return status;
-    CK(ce);
-    CK(cudaGraphInstantiate(&exec, graph, 0));
-    stamp("graph");
-    const auto t0 = now();
-    // the coder's column counter must start where the model does
-    for (long long i = warm; i < L; ++i) CK(cudaGraphLaunch(exec, m->s_main));
-    const auto t1 = now();
-    CK(cudaStreamSynchronize(m->s_main));
-    if (timing)
-      fprintf(stderr, "[fade] compress: %lld graph launches enqueued in %.3f s, done after %.3f s\n",
-              (long long)(L - warm), std::chrono::duration<double>(t1 - t0).count(),
-              std::chrono::duration<double>(now() - t0).count());
-    cudaGraphExecDestroy(exec);
-    stamp("execdestroy");
-    cudaGraphDestroy(graph);
-    stamp("gdestroy");
-    status = check_error(m, err);
-    stamp("checkerr");
-    if (status == FADE_OK && losses)
-      CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)(L - warm), cudaMemcpyDeviceToHost));
-    if (status == FADE_OK && alpha)
-      CK(cudaMemcpy(alpha, dalpha, sizeof(double) * 3 * (size_t)(L - warm), cudaMemcpyDeviceToHost));
-    stamp("losses");
-    dev_free(dloss, m->s_main);
-    dev_free(dalpha, m->s_main);
+    CK(dev_alloc((void**)&dloss, sizeof(double) * (size_t)nsteps, s));
+    if (alpha) CK(dev_alloc((void**)&dalpha, sizeof(double) * 3 * (size_t)nsteps, s));
+    if (tape) {
+      const size_t tb = sizeof(unsigned long long) * kTapeSlots * (size_t)nsteps;
+      CK(dev_alloc((void**)&dtape, tb, s));
+      CK(cudaMemsetAsync(dtape, 0, tb, s));
+      c->e.tape = dtape;
+      c->e.tape_base = warm;
+    }
+    CK(cudaStreamSynchronize(s));
+    // capture one timestep into a graph, replay it L - warm times (the coder's
+    // column counter starts where the model's does)
+    TRY(replay_steps(m, nsteps, dtape, [&] { return compress_step(m, c, mat, L, pipelined, dloss, dalpha); }));
+    c->e.tape = nullptr;
+    stamp("loop");
+    TRY(check_error(m, err));
+    if (losses) CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)nsteps, cudaMemcpyDeviceToHost));
+    if (alpha) CK(cudaMemcpy(alpha, dalpha, sizeof(double) * 3 * (size_t)nsteps, cudaMemcpyDeviceToHost));
+    if (tape)
+      CK(cudaMemcpy(tape, dtape, sizeof(unsigned long long) * kTapeSlots * (size_t)nsteps,
+                    cudaMemcpyDeviceToHost));
   }
-  stamp("loop");
   launch_encode_flush(c->e, batch, s);
   c->lengths.resize(batch);
   CK(cudaMemcpyAsync(c->lengths.data(), c->e.blen, sizeof(long long) * batch,
                      cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  dev_free(dmat, s);
-  CK(cudaStreamSynchronize(s));
   stamp("flush");
-  if (status != FADE_OK) return status;
   for (int b = 0; b < batch; ++b) lengths[b] = c->lengths[b];
   *coder_out = guard.release();
   return FADE_OK;
 }
 
-int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t nbytes,
+int fade_decompress(fade_model_t* m, int device, int batch, const uint8_t* payload, int64_t nbytes,
                     const int64_t* lengths, int64_t L, int64_t warm, uint8_t* out, double* losses,
-                    double* alpha, fade_error_t* err) {
+                    double* alpha, uint64_t* tape, fade_error_t* err) {
   if (m && m->d.B != batch) {
     set_last_error("decompress: batch does not match the model");
     return FADE_ERR_USAGE;
@@ -1237,8 +1301,8 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
     set_last_error("decompress: a model is required when L > warm");
     return FADE_ERR_USAGE;
   }
+  ON_DEVICE(m ? m->device : device);
   cudaStream_t s = m ? m->s_main : nullptr;
-  if (m) CK(cudaSetDevice(m->device));
   // device copies: payload, offsets, lengths, decoder state, output matrix
   std::vector<long long> off(batch);
   long long tot = 0;
@@ -1250,6 +1314,7 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
     set_last_error("decompress: payload length does not match the stream table");
     return FADE_ERR_USAGE;
   }
+  const long long nsteps = L > warm ? L - warm : 0;
   const size_t nB = (size_t)batch;
   const size_t sizes[8] = {(size_t)std::max<long long>(nbytes, 1), 8 * nB, 8 * nB, 8 * nB,
                            8 * nB, 8 * nB, (size_t)batch * (size_t)L + 1, 8};
@@ -1260,6 +1325,16 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
     total += sizes[i];
   }
   void* mem = nullptr;
+  double* dloss = nullptr;
+  double* dalpha = nullptr;
+  unsigned long long* dtape = nullptr;
+  auto cleanup = defer([&] {
+    dev_free(dloss, s);
+    dev_free(dalpha, s);
+    dev_free(dtape, s);
+    dev_free(mem, s);
+    cudaStreamSynchronize(s);
+  });
   CK(dev_alloc(&mem, total, s));
   char* base = (char*)mem;
   DecState ds;
@@ -1280,13 +1355,15 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
   }
   launch_dec_prime(ds, batch, err_key, s);
   launch_decode_warm(ds, batch, dmat, L, warm, err_key, s);
-  int status = FADE_OK;
-  double* dloss = nullptr;
-  double* dalpha = nullptr;
-  if (m && L > warm) {
+  if (m && nsteps > 0) {
     TRY(set_col(m, warm, warm));
-    CK(dev_alloc((void**)&dloss, sizeof(double) * (size_t)(L - warm), m->s_main));
-    if (alpha) CK(dev_alloc((void**)&dalpha, sizeof(double) * 3 * (size_t)(L - warm), m->s_main));
+    CK(dev_alloc((void**)&dloss, sizeof(double) * (size_t)nsteps, s));
+    if (alpha) CK(dev_alloc((void**)&dalpha, sizeof(double) * 3 * (size_t)nsteps, s));
+    if (tape) {
+      const size_t tb = sizeof(unsigned long long) * kTapeSlots * (size_t)nsteps;
+      CK(dev_alloc((void**)&dtape, tb, s));
+      CK(cudaMemsetAsync(dtape, 0, tb, s));
+    }
     StepIO io{};
     io.alpha_tape = dalpha;
     io.src = dmat;
@@ -1303,24 +1380,16 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
     io.head.dcode = ds.code;
     io.head.drng = ds.rng;
     io.head.adam_prep = 1;
-    cudaGraph_t graph;
-    cudaGraphExec_t exec;
-    CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
+    CK(cudaStreamSynchronize(s));
     // decode(i) -> train(i) -> predict(i+1) is strictly serial (pipeline.py:364-376)
-    status = forward(m, io, true);
-    if (status == FADE_OK) status = backward(m, io, false, dloss, 1);
-    cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
-    if (status != FADE_OK) return status;
-    CK(ce);
-    CK(cudaGraphInstantiate(&exec, graph, 0));
-    for (long long i = warm; i < L; ++i) CK(cudaGraphLaunch(exec, m->s_main));
-    CK(cudaStreamSynchronize(m->s_main));
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
+    TRY(replay_steps(m, nsteps, dtape, [&] {
+      int st = forward(m, io, true);
+      return st == FADE_OK ? backward(m, io, false, dloss, 1) : st;
+    }));
   }
   CK(cudaStreamSynchronize(s));
   if (m) {
-    status = check_error(m, err);
+    TRY(check_error(m, err));
   } else {
     unsigned long long key = 0;
     CK(cudaMemcpy(&key, err_key, 8, cudaMemcpyDeviceToHost));
@@ -1332,21 +1401,18 @@ int fade_decompress(fade_model_t* m, int batch, const uint8_t* payload, int64_t 
       err->step = code == 6 ? -1 : (long long)(key >> 24);
       set_last_error(code == 6 ? "stream shorter than coder tail"
                                : (code == 1 ? "invalid code value" : "truncated stream"));
-      status = FADE_ERR_CORRUPT;
+      return FADE_ERR_CORRUPT;
     }
   }
-  if (status == FADE_OK) {
-    CK(cudaMemcpy(out, dmat, (size_t)batch * (size_t)L, cudaMemcpyDeviceToHost));
-    if (losses && dloss)
-      CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)(L - warm), cudaMemcpyDeviceToHost));
-    if (alpha && dalpha)
-      CK(cudaMemcpy(alpha, dalpha, sizeof(double) * 3 * (size_t)(L - warm), cudaMemcpyDeviceToHost));
-  }
-  if (dloss) dev_free(dloss, m->s_main);
-  if (dalpha) dev_free(dalpha, m->s_main);
-  dev_free(mem, s);
-  cudaStreamSynchronize(s);
-  return status;
+  CK(cudaMemcpy(out, dmat, (size_t)batch * (size_t)L, cudaMemcpyDeviceToHost));
+  if (losses && dloss)
+    CK(cudaMemcpy(losses, dloss, sizeof(double) * (size_t)nsteps, cudaMemcpyDeviceToHost));
+  if (alpha && dalpha)
+    CK(cudaMemcpy(alpha, dalpha, sizeof(double) * 3 * (size_t)nsteps, cudaMemcpyDeviceToHost));
+  if (tape && dtape)
+    CK(cudaMemcpy(tape, dtape, sizeof(unsigned long long) * kTapeSlots * (size_t)nsteps,
+                  cudaMemcpyDeviceToHost));
+  return FADE_OK;
 }
 
 int fade_model_stream(fade_model_t* m, void** stream) {
@@ -1356,7 +1422,7 @@ int fade_model_stream(fade_model_t* m, void** stream) {
 
 int fade_bench_probe(fade_model_t* m, int which, int iters, double* ms, double* bytes,
                      double* flops) {
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   const Dims& d = m->d;
   const double B = d.B, H = d.H, Ep = d.Ep, C = d.C, X = d.X;
   auto launch = [&]() -> int {
@@ -1412,9 +1478,9 @@ int fade_bench_probe(fade_model_t* m, int which, int iters, double* ms, double* 
 int fade_bench_compress_steps(fade_model_t* m, const uint8_t* data_dev, int64_t L, int64_t start,
                               int64_t steps, fade_coder_t** coder, int* launches, void* stream) {
   (void)stream;
-  CK(cudaSetDevice(m->device));
+  ON_DEVICE(m->device);
   if (!*coder) {
-    TRY(coder_create(m->d.B, L, m->s_main, coder));
+    TRY(coder_create(m->d.B, L, m->device, m->s_main, coder));
     TRY(set_col(m, start, start));
     long long v = start;
     CK(cudaMemcpy((*coder)->e.col, &v, sizeof(v), cudaMemcpyHostToDevice));

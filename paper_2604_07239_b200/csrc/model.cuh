@@ -114,7 +114,13 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   int splits_mem, splits_f, splits_dz2;
   SplitBuf sk[S_COUNT];
   double lr, beta1, beta2, adam_eps;   // Adam hyperparameters (config.py:29-32)
+  // executors only: device event tape [steps][kTapeSlots] indexed by
+  // col - loss_base (null: not recorded)
+  unsigned long long* tape;
 };
+__device__ __forceinline__ unsigned long long* tape_at(const ModelPtrs& M, int slot) {
+  return M.tape + kTapeSlots * (M.st->col - M.st->loss_base) + slot;
+}
 
 // row kernels (model_kernels.cu)
 void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
 
   const VFlags vf = vflags(M.variant);
   const long long c0 = use_col ? M.st->col - d.T : 0;
+  if (M.tape && b == 0 && tid == 0) *tape_at(M, 0) = gtimer_ns();
   float* crow = M.a.cache + (long long)b * d.C;
   const int n4 = (d.C - d.D) / 4;        // float4 count the roll moves
   if constexpr (DT > 0) {
@@ -614,6 +615,17 @@ __device__ __forceinline__ double block_sum_d256(double v, double* red) {
 
 __device__ void adam_prep_dev(StepState* st, double lr, double b1, double b2, double eps);
 
+// After a divergence or quantiser failure the graph keeps replaying the
+// remaining timesteps (the host reads the error once, at the end), so the
+// failing row's table slot gets the uniform table (coder.py:46-49): the
+// encoder downstream then codes a well-formed interval instead of reading a
+// stale or zero-width slot.  The run's result is the recorded error.
+__device__ __forceinline__ void write_uniform_cum(unsigned* cum) {
+  const int i = threadIdx.x;
+  cum[i] = (unsigned)i * 256u;
+  if (i == kAlphabet - 1) cum[kAlphabet] = kTotal;
+}
+
 // fp64 softmax of one 256-logit row, thread i = symbol i: row max in float
 // (exact), z = logit - max in f64, p = exp(z) / sum.  The head kernel and the
 // coder-stream quantiser (k_head_quant) both use this exact sequence, so the
@@ -655,6 +667,7 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
     adam_prep_dev(st, M.lr, M.beta1, M.beta2, M.adam_eps);
   if (bad_s) {
     if (i == 0) record_error(st, col, b, 3);
+    if (!H.skip_quant) write_uniform_cum(M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd);
     return;
   }
   __shared__ float fred[8];
@@ -664,12 +677,13 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
   if (!H.skip_quant) {
     bool qbad;
     const int f = quantize_sym(p, qs, &qbad);
+    unsigned* cum = M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd;
     if (qbad) {
       if (i == 0) record_error(st, col, b, 4);
+      write_uniform_cum(cum);
       return;
     }
     const int c = block_excl_scan256(f, wsum);
-    unsigned* cum = M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd;
     cum[i] = (unsigned)c;
     cum_s[i] = (unsigned)c;
     if (i == kAlphabet - 1) {
@@ -677,6 +691,7 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
       cum_s[kAlphabet] = kTotal;
     }
     __syncthreads();
+    if (M.tape && i == 0) atomicMax(tape_at(M, 1), gtimer_ns());
   }
   if (!H.xent) return;
   int tgt;
@@ -695,6 +710,11 @@ __global__ void __launch_bounds__(256) k_head(ModelPtrs M, HeadArgs H) {
       }
       H.out[(long long)b * H.ld_out + col] = (uint8_t)sy;
       sym_s = sy;
+      if (M.tape) {
+        // the decoder drains the table inside this kernel
+        if (b == 0) *tape_at(M, 2) = gtimer_ns();
+        atomicMax(tape_at(M, 3), gtimer_ns());
+      }
     }
     __syncthreads();
     tgt = sym_s;
@@ -736,19 +756,24 @@ __global__ void __launch_bounds__(256) k_head_quant(ModelPtrs M, const long long
   __syncthreads();
   if (!isfinite(lg)) atomicOr(&bad_s, 1);
   __syncthreads();
-  if (bad_s) return;      // the head kernel has recorded the divergence
+  unsigned* cum = M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd;
+  if (bad_s) {            // the head kernel has recorded the divergence
+    write_uniform_cum(cum);
+    return;
+  }
   double z, s;
   const double p = row_softmax(lg, fred, dred, &z, &s);
   bool qbad;
   const int f = quantize_sym(p, qs, &qbad);
   if (qbad) {
     if (i == 0) record_error(M.st, col, b, 4);
+    write_uniform_cum(cum);
     return;
   }
   const int c = block_excl_scan256(f, wsum);
-  unsigned* cum = M.a.cum + ((col & 1) * (long long)M.d.B + b) * kCumLd;
   cum[i] = (unsigned)c;
   if (i == kAlphabet - 1) cum[kAlphabet] = kTotal;
+  if (M.tape && i == 0) atomicMax(M.tape + kTapeSlots * (col - M.st->loss_base) + 1, gtimer_ns());
 }
 
 void launch_head_quant(const ModelPtrs& M, const long long* colp, cudaStream_t s) {
@@ -1486,6 +1511,7 @@ __global__ void __maxnreg__(40) k_small_adam(ModelPtrs M, int grad_only,
       StepState* st = M.st;
       if (!isfinite(l)) record_error(st, st->col, 0, 5);
       if (losses) losses[st->col - st->loss_base] = l;
+      if (M.tape) *tape_at(M, 4) = gtimer_ns();
       if (alpha_tape) {
         double* rec = alpha_tape + 3 * (st->col - st->loss_base);
         rec[0] = as / ((double)M.d.B * M.d.H);

@@ -58,16 +58,23 @@ __global__ void k_encode_col(EncState e, int B, const uint8_t* data, long long l
   pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   const long long col = *e.col;
+  if (e.tape && b == 0) e.tape[kTapeSlots * (col - e.tape_base) + 2] = gtimer_ns();
   if (b < B) {
     const unsigned* row = cum + ((col & 1) * (long long)B + b) * kCumLd;
     const unsigned sym = data[(long long)b * ld + col];
     EncLane s = load_lane(e, b);
-    enc_symbol(s, row[sym], row[sym + 1], e.buf + (long long)b * e.cap);
+    unsigned c0 = row[sym], c1 = row[sym + 1];
+    // memory safety only: every quantised table has freq >= 1, so a
+    // zero-width interval means the step already failed (error recorded);
+    // code the uniform interval instead of renormalising without bound
+    if (c1 <= c0) c0 = sym * 256u, c1 = c0 + 256u;
+    enc_symbol(s, c0, c1, e.buf + (long long)b * e.cap);
     store_lane(e, b, s);
   }
   // the last block to finish advances the column (every block has read it)
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (e.tape) atomicMax(e.tape + kTapeSlots * (col - e.tape_base) + 3, gtimer_ns());
     __threadfence();
     const unsigned prev = atomicAdd(e.done_blocks, 1u);
     if (prev == gridDim.x - 1) {

@@ -16,6 +16,8 @@ struct EncState {
   long long cap;
   long long* col;          // column the next encode launch codes
   unsigned* done_blocks;   // last-block-done counter for advancing *col
+  unsigned long long* tape; // executor event tape (model.cuh kTapeSlots), or null
+  long long tape_base;      // column of tape row 0
 };
 
 struct DecState {

@@ -1,4 +1,5 @@
 // ABI housekeeping: error strings, version, and a GEMM test hook.
+#include <cstring>
 #include <string>
 
 #include "../../include/fade_b200.h"
@@ -16,12 +17,27 @@ extern "C" {
 
 const char* fade_last_error(void) { return last_error(); }
 
-int fade_abi_version(void) { return 2; }
+int fade_abi_version(void) { return 3; }
 
 int fade_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
   return n;
+}
+
+int fade_device_arch(int device, int* major, int* minor, char* name, int name_len) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    set_last_error("fade_device_arch: no such device");
+    return FADE_ERR_CUDA;
+  }
+  *major = prop.major;
+  *minor = prop.minor;
+  if (name && name_len > 0) {
+    strncpy(name, prop.name, (size_t)name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  return FADE_OK;
 }
 
 // Test hook for the tcgen05 GEMM (device pointers, fp32 in/out, TF32 math):

@@ -17,6 +17,8 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
+import sys
 
 import numpy as np
 
@@ -54,27 +56,31 @@ def _shapes(cfg: ModelConfig) -> dict:
     return shapes
 
 
-_INIT_CACHE: dict = {}
-
-
 def init_params(cfg: ModelConfig) -> dict:
     """numpy ``default_rng(seed)`` draws in the reference order (model.py:62-105).
 
-    The draw is a pure function of the geometry and the seed and costs ~0.2 s
-    at the default size, so the last result is kept (read-only arrays) for
-    repeated ``compress_bytes`` / ``Predictor`` calls with the same config.
+    Drawn afresh on every call, as the reference does for every Predictor
+    (~0.2 s at the default size; part of every timed compress_bytes call).
     """
-    key = (cfg.ctx_len, cfg.embed_dim, cfg.cache_dim, cfg.mix_dim, cfg.expand_dim, cfg.batch,
-           cfg.alphabet, cfg.conv_kernel, cfg.seed)
-    hit = _INIT_CACHE.get(key)
-    if hit is not None:
-        return hit
-    out = _draw_params(cfg)
-    for a in out.values():
-        a.flags.writeable = False
-    _INIT_CACHE.clear()
-    _INIT_CACHE[key] = out
-    return out
+    return _draw_params(cfg)
+
+
+def default_device() -> int:
+    """The CUDA device a model lands on when the caller names none.
+
+    torch's current device when torch has initialised CUDA in this process
+    (``torch.cuda.set_device(local_rank)`` under torchrun), else
+    ``LOCAL_RANK`` (one process per GPU), else 0.  The native calls restore
+    the caller's current device, so this choice never leaks into torch.
+    """
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_initialized():
+                return int(torch.cuda.current_device())
+        except Exception:  # noqa: BLE001 - a broken torch install must not matter here
+            pass
+    return int(os.environ.get("LOCAL_RANK", "0"))
 
 
 def _draw_params(cfg: ModelConfig) -> dict:
@@ -112,7 +118,7 @@ def _ptr(a: np.ndarray):
 class Predictor:
     """One device model driving all B streams (model.py:44-58)."""
 
-    def __init__(self, cfg: ModelConfig, variant: str = "full", device: int = 0):
+    def __init__(self, cfg: ModelConfig, variant: str = "full", device: int | None = None):
         cfg.validate()
         if variant not in VARIANTS:
             raise UsageError(f"unknown variant {variant!r}, pick one of {VARIANTS}")
@@ -120,7 +126,8 @@ class Predictor:
         _native.require_device()
         self.cfg = cfg
         self.variant = variant
-        self.device = device
+        self.device = default_device() if device is None else int(device)
+        device = self.device
         self._shapes = _shapes(cfg)
         lib = _native.lib()
         h = ctypes.c_void_p()

@@ -16,7 +16,6 @@ because the table for step i is always built before the step-i update.
 from __future__ import annotations
 
 import ctypes
-import threading
 import time
 from dataclasses import dataclass, field
 
@@ -25,7 +24,7 @@ import numpy as np
 from . import _native
 from .config import ModelConfig
 from .errors import CorruptionError, ModelDivergenceError
-from .model import LN2, Predictor
+from .model import LN2, Predictor, default_device
 
 __all__ = [
     "StreamPartition",
@@ -72,21 +71,25 @@ _LEGAL = {("empty", "filling"), ("filling", "full"), ("full", "draining"), ("dra
 
 
 class PingPongBuffer:
-    """The two-slot handoff protocol of pipeline.py:67-149, host side.
+    """The two-slot handoff of pipeline.py:67-149 (empty -> filling -> full ->
+    draining -> empty), as the device ran it.
 
-    The device executor implements this protocol with CUDA events (model
-    stream records "full" after the head kernel writes slot i%2; the coder
-    stream waits on it, encodes, and records "empty").  This class keeps the
-    reference's host API so a host-thread producer/consumer can still use it,
-    and it replays the device schedule into a ``trace`` callback.
+    On the B200 the handoff is two CUDA events per timestep: the model stream
+    records "full" once the quantiser has written slot ``i % 2`` and the
+    coder stream waits on it, encodes and records "empty", which the model
+    stream waits on before it reuses the slot.  The kernels stamp each of
+    those moments with the device clock into the executor's event tape
+    (``fade_compress`` ``tape``: fill begins, table full, drain begins, drain
+    done per step).  ``replay_tape`` feeds the recorded transitions through
+    the reference's legality check in device-time order, so a ``trace``
+    callback observes the schedule that actually ran -- including warm-up
+    steps, whose uniform tables the warm-up kernel codes before the first
+    model step.
     """
 
     def __init__(self, trace=None):
         self._states = ["empty", "empty"]
-        self._cond = threading.Condition()
         self._trace = trace
-        self._exc: BaseException | None = None
-        self._payload: list = [None, None]
 
     def _set(self, slot: int, new: str) -> None:
         old = self._states[slot]
@@ -95,55 +98,28 @@ class PingPongBuffer:
         if self._trace is not None:
             self._trace((slot, old, new))
 
-    def _wait(self, slot: int, state: str) -> None:
-        with self._cond:
-            while self._states[slot] != state:
-                if self._exc is not None:
-                    raise self._exc
-                self._cond.wait(timeout=0.1)
-
-    def acquire_fill(self, step: int) -> int:
-        slot = step % 2
-        self._wait(slot, "empty")
-        with self._cond:
-            self._set(slot, "filling")
-        return slot
-
-    def commit_fill(self, slot: int, payload=None) -> None:
-        with self._cond:
-            self._payload[slot] = payload
-            self._set(slot, "full")
-            self._cond.notify_all()
-
-    def acquire_drain(self, step: int) -> int:
-        slot = step % 2
-        self._wait(slot, "full")
-        with self._cond:
-            self._set(slot, "draining")
-        return slot
-
-    def commit_drain(self, slot: int) -> None:
-        with self._cond:
-            self._payload[slot] = None
-            self._set(slot, "empty")
-            self._cond.notify_all()
-
-    def payload(self, slot: int):
-        return self._payload[slot]
-
-    def abort(self, exc: BaseException) -> None:
-        with self._cond:
-            if self._exc is None:
-                self._exc = exc
-            self._cond.notify_all()
-
-    def replay(self, steps: int) -> None:
-        """Emit the device schedule's slot transitions for ``steps`` timesteps."""
-        for i in range(steps):
-            s = self.acquire_fill(i)
-            self.commit_fill(s)
-            s = self.acquire_drain(i)
-            self.commit_drain(s)
+    def replay_tape(self, warm: int, tape) -> list:
+        """Replay ``warm`` uniform-table steps, then the device tape
+        ([steps, 5] int64 ns).  Returns the (t_ns, step, slot, new_state)
+        events in the order they were applied."""
+        events = []
+        for i in range(warm):            # coded back to back by k_encode_warm
+            for st in ("filling", "full", "draining", "empty"):
+                events.append((0, i, i % 2, st))
+        tape = np.asarray(tape, dtype=np.int64).reshape(-1, 5) if tape is not None else \
+            np.zeros((0, 5), np.int64)
+        timed = []
+        for k, row in enumerate(tape):
+            i = warm + k
+            for st, t in zip(("filling", "full", "draining", "empty"), row[:4]):
+                timed.append((int(t), i, i % 2, st))
+        # device-time order; a tie keeps the protocol order of one step
+        order = {"filling": 0, "full": 1, "draining": 2, "empty": 3}
+        timed.sort(key=lambda e: (e[0], e[1], order[e[3]]))
+        events += timed
+        for _, _, slot, st in events:
+            self._set(slot, st)
+        return events
 
 
 @dataclass
@@ -154,21 +130,22 @@ class CompressResult:
     losses: list = field(default_factory=list)
     elapsed: float = 0.0
     metrics: list | None = None
+    device: int | None = None     # CUDA device that ran the model (v2 shard fingerprint)
 
 
-def _metrics(phase: str, first_step: int, losses, elapsed: float, bytes_per_step: int,
-             alpha=None) -> list:
+def _metrics(phase: str, first_step: int, losses, bytes_per_step: int, alpha=None,
+             tape=None) -> list:
     """Per-step records of the --metrics tape (pipeline.py:162-185).
 
-    Losses and the router statistics (mean, min, max of alpha, model.py:197-199)
-    come from the device, one row per model step; the per-step wall clock is the
-    device run's elapsed time spread uniformly (the graph replay has no
-    host-visible steps).
+    Loss, router statistics (mean, min, max of alpha, model.py:197-199) and the
+    clock all come from the device: ``elapsed_s`` is the %globaltimer time
+    from the start of the first model step to the end of this one (event
+    tape slot 4), so per-step timing is measured, not interpolated.
     """
-    n = len(losses)
+    t = np.asarray(tape, dtype=np.int64).reshape(-1, 5) if tape is not None else None
     recs = []
     for k, loss in enumerate(losses):
-        el = elapsed * (k + 1) / max(n, 1)
+        el = float(t[k, 4] - t[0, 0]) * 1e-9 if t is not None else 0.0
         rec = {"phase": phase, "step": first_step + k, "loss_nats": float(loss),
                "bits_per_byte": float(loss) / LN2, "elapsed_s": el,
                "kb_per_min": ((first_step + k + 1) * bytes_per_step / 1024.0)
@@ -200,13 +177,14 @@ def _raise_device(status: int, err: _native.FadeError, what: str):
 
 
 def _compress(data: bytes, cfg: ModelConfig, variant: str, pipelined: bool,
-              collect_metrics: bool, trace=None) -> CompressResult:
+              collect_metrics: bool, trace=None, device=None) -> CompressResult:
     t0 = time.perf_counter()
     if not data:
         return CompressResult([], cfg, StreamPartition.from_length(0, cfg.batch))
     cfg, part, mat, warm = _prepare(data, cfg)
     steps = part.stream_length
-    model = Predictor(cfg, variant) if steps > warm else None
+    dev = default_device() if device is None else int(device)
+    model = Predictor(cfg, variant, device=dev) if steps > warm else None
     if model is None:
         _native.require_device()
     lib = _native.lib()
@@ -218,9 +196,12 @@ def _compress(data: bytes, cfg: ModelConfig, variant: str, pipelined: bool,
     mat = np.ascontiguousarray(mat)
     routed = variant not in ("global_only", "local_only")   # alpha exists (model.py:146-151)
     alpha = np.zeros((max(nsteps, 1), 3), dtype=np.float64) if collect_metrics and routed else None
-    st = lib.fade_compress(model.handle if model else None, cfg.batch, mat.ctypes.data, steps,
-                           warm, 0, 1 if pipelined else 0, lengths.ctypes.data, losses.ctypes.data,
-                           alpha.ctypes.data if alpha is not None else None,
+    want_tape = collect_metrics or trace is not None
+    tape = np.zeros((max(nsteps, 1), 5), dtype=np.uint64) if want_tape else None
+    st = lib.fade_compress(model.handle if model else None, dev, cfg.batch, mat.ctypes.data,
+                           steps, warm, 0, 1 if pipelined else 0, lengths.ctypes.data,
+                           losses.ctypes.data, alpha.ctypes.data if alpha is not None else None,
+                           tape.ctypes.data if tape is not None else None,
                            ctypes.byref(coder), ctypes.byref(err))
     if st != 0:
         _raise_device(st, err, "fade_compress")
@@ -234,29 +215,36 @@ def _compress(data: bytes, cfg: ModelConfig, variant: str, pipelined: bool,
     streams = [payload[offs[k]:offs[k + 1]].tobytes() for k in range(cfg.batch)]
     loss_list = [float(x) for x in losses[:nsteps]] if nsteps > 0 else []
     elapsed = time.perf_counter() - t0
+    tape_rows = tape[:nsteps].astype(np.int64) if tape is not None and nsteps > 0 else None
     if trace is not None:
-        PingPongBuffer(trace).replay(steps)
-    metrics = (_metrics("compress", warm, loss_list, elapsed, cfg.batch,
-                        alpha if model is not None else None)
+        PingPongBuffer(trace).replay_tape(warm, tape_rows)
+    metrics = (_metrics("compress", warm, loss_list, cfg.batch,
+                        alpha if model is not None else None, tape_rows)
                if collect_metrics else None)
-    return CompressResult(streams, cfg, part, loss_list, elapsed, metrics)
+    return CompressResult(streams, cfg, part, loss_list, elapsed, metrics, dev)
 
 
 def run_serial_compress(data: bytes, cfg: ModelConfig, variant: str = "full",
-                        coder_delay: float = 0.0, collect_metrics: bool = False) -> CompressResult:
+                        coder_delay: float = 0.0, collect_metrics: bool = False,
+                        device: int | None = None) -> CompressResult:
     """predict -> quantise -> encode -> train per step, one CUDA stream (pipeline.py:197-226).
 
     ``coder_delay`` (the reference's latency injection) has no device analogue
-    and is accepted for API compatibility only.
+    and is accepted for API compatibility only.  ``device``: the CUDA device
+    to run on (default: ``model.default_device()``).
     """
-    return _compress(data, cfg, variant, False, collect_metrics)
+    return _compress(data, cfg, variant, False, collect_metrics, device=device)
 
 
 def run_pipelined_compress(data: bytes, cfg: ModelConfig, variant: str = "full",
                            coder_delay: float = 0.0, collect_metrics: bool = False,
-                           trace=None) -> CompressResult:
-    """CSPP: coder stream double-buffered against the model stream (pipeline.py:229-299)."""
-    return _compress(data, cfg, variant, True, collect_metrics, trace)
+                           trace=None, device: int | None = None) -> CompressResult:
+    """CSPP: coder stream double-buffered against the model stream (pipeline.py:229-299).
+
+    ``trace`` receives the (slot, old, new) transitions of the two-slot
+    buffer in the order the device ran them (``PingPongBuffer.replay_tape``).
+    """
+    return _compress(data, cfg, variant, True, collect_metrics, trace, device)
 
 
 def clamp_workers(workers: int, n_streams: int) -> int:
@@ -270,7 +258,7 @@ def clamp_workers(workers: int, n_streams: int) -> int:
 def run_parallel_decompress(payload: np.ndarray, offsets: np.ndarray, lengths: np.ndarray,
                             cfg: ModelConfig, original_length: int, workers: int = 1,
                             decode_delay: float = 0.0, want_losses: bool = False,
-                            collect_metrics: bool = False):
+                            collect_metrics: bool = False, device: int | None = None):
     """Decode every stream while replaying the encoder's updates (pipeline.py:310-396).
 
     One lane per stream replaces the reference's worker threads and their two
@@ -278,12 +266,12 @@ def run_parallel_decompress(payload: np.ndarray, offsets: np.ndarray, lengths: n
     """
     if original_length == 0:
         return (b"", []) if want_losses else b""
-    t0 = time.perf_counter()
     clamp_workers(workers, cfg.batch)
     part = StreamPartition.from_length(original_length, cfg.batch)
     steps = part.stream_length
     warm = min(cfg.ctx_len, steps)
-    model = Predictor(cfg) if steps > warm else None
+    dev = default_device() if device is None else int(device)
+    model = Predictor(cfg, device=dev) if steps > warm else None
     if model is None:
         _native.require_device()
     pay = np.asarray(payload, dtype=np.uint8)
@@ -299,12 +287,14 @@ def run_parallel_decompress(payload: np.ndarray, offsets: np.ndarray, lengths: n
     nsteps = steps - warm
     losses = np.zeros(max(nsteps, 1), dtype=np.float64)
     alpha = np.zeros((max(nsteps, 1), 3), dtype=np.float64) if collect_metrics else None
+    tape = np.zeros((max(nsteps, 1), 5), dtype=np.uint64) if collect_metrics else None
     err = _native.FadeError()
-    st = _native.lib().fade_decompress(model.handle if model else None, cfg.batch,
+    st = _native.lib().fade_decompress(model.handle if model else None, dev, cfg.batch,
                                        pay.ctypes.data if pay.size else None, pay.size,
                                        lengths.ctypes.data, steps, warm, out.ctypes.data,
                                        losses.ctypes.data,
                                        alpha.ctypes.data if alpha is not None else None,
+                                       tape.ctypes.data if tape is not None else None,
                                        ctypes.byref(err))
     if st != 0:
         _raise_device(st, err, "fade_decompress")
@@ -313,8 +303,9 @@ def run_parallel_decompress(payload: np.ndarray, offsets: np.ndarray, lengths: n
     if want_losses:
         return data, loss_list
     if collect_metrics:
-        return data, _metrics("decompress", warm, loss_list, time.perf_counter() - t0, cfg.batch,
-                              alpha if model is not None else None)
+        rows = tape[:nsteps].astype(np.int64) if nsteps > 0 else None
+        return data, _metrics("decompress", warm, loss_list, cfg.batch,
+                              alpha if model is not None else None, rows)
     return data
 
 

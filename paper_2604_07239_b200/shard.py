@@ -29,51 +29,61 @@ def shard_bounds(n: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
-def compress_shard(data: bytes, cfg: ModelConfig, rank: int, world: int, compress_fn=None):
-    """Compress this rank's chunk; returns its CompressResult."""
+def compress_shard(data: bytes, cfg: ModelConfig, rank: int, world: int, compress_fn=None,
+                   device: int | None = None):
+    """Compress this rank's chunk on ``device`` (default: this rank's
+    ``model.default_device()``, i.e. LOCAL_RANK); returns its CompressResult."""
     from .pipeline import run_pipelined_compress
     lo, hi = shard_bounds(len(data), world)[rank]
-    fn = compress_fn or run_pipelined_compress
-    return fn(data[lo:hi], cfg)
+    if compress_fn is not None:
+        return compress_fn(data[lo:hi], cfg)
+    return run_pipelined_compress(data[lo:hi], cfg, device=device)
 
 
-def compress_sharded(data: bytes, cfg: ModelConfig, group=None, compress_fn=None) -> bytes | None:
+def compress_sharded(data: bytes, cfg: ModelConfig, group=None, compress_fn=None,
+                     device: int | None = None, fingerprint_fn=None) -> bytes | None:
     """Collective entry point: every rank calls it with the same `data`.
 
-    Returns the v2 container on rank 0 and None elsewhere.  Each rank's device
-    must already be selected (`torch.cuda.set_device(local_rank)`).
+    Returns the v2 container on rank 0 and None elsewhere.  Each rank runs
+    its shard on ``device`` (default: its own LOCAL_RANK GPU) and stamps it
+    with its own ``shard_fingerprint`` (build + GPU architecture).
     """
     import torch.distributed as dist
 
     from . import container
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    res = compress_shard(data, cfg, rank, world, compress_fn)
+    res = compress_shard(data, cfg, rank, world, compress_fn, device)
+    fp_fn = fingerprint_fn or (lambda c: container.shard_fingerprint(c, res.device or 0))
     # host-side gather of (stream table, bytes) -- the only exchange step
-    payload = (res.partition.original_length, res.cfg, [bytes(s) for s in res.streams], res.losses)
+    payload = (res.partition.original_length, res.cfg, [bytes(s) for s in res.streams], res.losses,
+               fp_fn(res.cfg))
     gathered = [None] * world if rank == 0 else None
     dist.gather_object(payload, gathered, dst=0, group=group)
     if rank != 0:
         return None
     from .pipeline import CompressResult, StreamPartition
-    results = []
-    for orig, rcfg, streams, losses in gathered:
+    results, fps = [], []
+    for orig, rcfg, streams, losses, fp in gathered:
         rcfg = rcfg or replace(cfg, batch=max(1, len(streams)))
         results.append(CompressResult(streams, rcfg, StreamPartition.from_length(orig, len(streams)),
                                       losses))
-    return container.pack_shards(results, cfg)
+        fps.append(fp)
+    return container.pack_shards(results, cfg, fps)
 
 
-def decompress_sharded(blob: bytes, group=None) -> bytes | None:
-    """Each rank decodes its share of the shards; rank 0 returns the bytes."""
+def decompress_sharded(blob: bytes, group=None, device: int | None = None,
+                       decompress_fn=None) -> bytes | None:
+    """Each rank decodes its share of the shards on its own device; rank 0
+    returns the bytes."""
     import torch.distributed as dist
 
     from . import container
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     shards = container.unpack_shards(blob)
-    mine = {i: container.decompress_shard(s, fp) for i, (s, fp) in enumerate(shards)
-            if i % world == rank}
+    fn = decompress_fn or (lambda s, fp: container.decompress_shard(s, fp, device=device))
+    mine = {i: fn(s, fp) for i, (s, fp) in enumerate(shards) if i % world == rank}
     gathered = [None] * world if rank == 0 else None
     dist.gather_object(mine, gathered, dst=0, group=group)
     if rank != 0:

@@ -65,11 +65,43 @@ def test_partition_round_trip():
 
 
 def test_pingpong_protocol_trace():
+    """Replaying a device event tape: warm-up steps first, then the model
+    steps in device-time order; every slot follows the legal cycle."""
     seen = []
-    PingPongBuffer(seen.append).replay(3)
+    # two model steps after 2 warm-up steps; step 3 fills while 2 still drains?
+    # no: the model stream waits for the drain of step i before step i+1
+    tape = np.array([[100, 110, 111, 115, 130],
+                     [131, 140, 141, 144, 160]], np.int64)
+    ev = PingPongBuffer(seen.append).replay_tape(2, tape)
     assert seen[:4] == [(0, "empty", "filling"), (0, "filling", "full"),
                         (0, "full", "draining"), (0, "draining", "empty")]
-    assert len(seen) == 12
+    assert len(seen) == 16
+    assert [e[1] for e in ev[8:]] == [2] * 4 + [3] * 4
+    assert [s for s, _, _ in seen[8:12]] == [0] * 4 and [s for s, _, _ in seen[12:]] == [1] * 4
+
+
+def test_pingpong_rejects_an_illegal_tape():
+    """A tape where slot 0 is refilled before it drained fails the reference's
+    transition check (pipeline.py:78-83)."""
+    tape = np.array([[100, 110, 150, 160, 170],
+                     [120, 125, 126, 127, 128],
+                     [130, 135, 136, 137, 138]], np.int64)   # step 2 (slot 0) fills at 130 < 150
+    with pytest.raises(AssertionError):
+        PingPongBuffer().replay_tape(0, tape)
+
+
+def test_product_init_matches_reference_default_digest():
+    """The product's seeded draw (model.init_params, uploaded by every
+    Predictor) equals the reference's default-config init byte for byte."""
+    import hashlib
+    import json
+    from paper_2604_07239_b200.config import ModelConfig
+    from paper_2604_07239_b200.model import PARAM_ORDER, init_params
+    z = load_golden("model_default_digest.npz")
+    dig = json.loads(bytes(z["digest_json"]).decode())
+    p = init_params(ModelConfig(seed=5))
+    for k in PARAM_ORDER:
+        assert hashlib.sha256(p[k].tobytes()).hexdigest() == dig[k], k
 
 
 class TestContainer:
@@ -130,7 +162,7 @@ class TestContainer:
         for k in range(3):
             streams = [bytes([k, j]) * (j + 2) for j in range(4)]
             res.append(CompressResult(streams, cfg, StreamPartition.from_length(10 + k, 4)))
-        blob = container.pack_shards(res, cfg)
+        blob = container.pack_shards(res, cfg, [1, 2, 3])
         shards = container.unpack_shards(blob)
         assert [s.original_length for s, _ in shards] == [10, 11, 12]
         assert shards[2][0].payload == b"".join(res[2].streams)
@@ -154,7 +186,7 @@ def test_abi_library_exports_every_declared_symbol():
     missing = [s for s in declared if not hasattr(so, s)]
     assert not missing
     assert declared == set(_native.SIGNATURES)
-    assert so.fade_abi_version() == 2
+    assert so.fade_abi_version() == 3
 
 
 def test_active_params_match_reference_gradients():

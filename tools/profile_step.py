@@ -5,8 +5,9 @@ from paper_2604_07239_b200 import ModelConfig, _native, corpus
 from paper_2604_07239_b200.model import Predictor
 from paper_2604_07239_b200.pipeline import StreamPartition
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-cfg = ModelConfig(batch=512, workers=1)
-data = corpus.make_text(4_000_000, 12)
+batch = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+cfg = ModelConfig(batch=batch, workers=1)
+data = corpus.make_text(max(4_000_000, batch * 64), 12)
 part = StreamPartition.from_length(len(data), cfg.batch)
 mat = np.ascontiguousarray(part.split(data)); L = part.stream_length
 dmat = torch.from_numpy(mat).cuda()

@@ -2,7 +2,7 @@
 torch.profiler): per-kernel start offset, duration and stream for one
 timestep, plus per-kernel mean durations over the profiled steps.
 
-    python tools/timeline.py [steps] > timeline.txt
+    python tools/timeline.py [steps] [batch] > timeline.txt
 """
 import ctypes
 import json
@@ -22,8 +22,9 @@ def main():
     from paper_2604_07239_b200.model import Predictor
     from paper_2604_07239_b200.pipeline import StreamPartition
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 16
-    cfg = ModelConfig(batch=512, workers=1)
-    data = corpus.make_text(2_000_000, 12)
+    batch = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+    cfg = ModelConfig(batch=batch, workers=1)
+    data = corpus.make_text(max(2_000_000, batch * (n + 80)), 12)
     part = StreamPartition.from_length(len(data), cfg.batch)
     mat = np.ascontiguousarray(part.split(data))
     L = part.stream_length

@@ -27,12 +27,23 @@ oracle:
 PROBE_OBJS := $(patsubst $(SRC_DIR)/%.cu,build/probe/%.o,$(SRCS))
 build/probe/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p build/probe
-	$(NVCC) $(NVFLAGS) -DFADE_PHASE_PROBE -dc -o $@ $< 2> build/probe/$*.ptxas.log || (cat build/probe/$*.ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -DFADE_PHASE_PROBE -DFADE_EXPERIMENTS -dc -o $@ $< 2> build/probe/$*.ptxas.log || (cat build/probe/$*.ptxas.log; exit 1)
 build/probe/libfade_b200.so: $(PROBE_OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@ $(PROBE_OBJS)
 probe: build/probe/libfade_b200.so
 
+# experiments build: reads the FADE_* tuning / debug knobs from the
+# environment (common.cuh knob()); load it with FADE_LIB_PATH for A/B timing.
+# The shipped library above ignores them.
+EXP_OBJS := $(patsubst $(SRC_DIR)/%.cu,build/exp/%.o,$(SRCS))
+build/exp/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p build/exp
+	$(NVCC) $(NVFLAGS) -DFADE_EXPERIMENTS -dc -o $@ $< 2> build/exp/$*.ptxas.log || (cat build/exp/$*.ptxas.log; exit 1)
+build/exp/libfade_b200.so: $(EXP_OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -Xcompiler -fPIC -o $@ $(EXP_OBJS)
+experiments: build/exp/libfade_b200.so
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean oracle probe
+.PHONY: all clean oracle probe experiments

@@ -3,21 +3,26 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE.json config 2): FADE default model (ModelConfig(): B = 512
-streams, 24 M parameters, online Adam) on a seeded 100 MB enwik8-shaped text
-stream (``corpus.make_text(100_000_000, 12)``), one byte per stream per
-timestep.  One bench "step" = ``--chunk`` timesteps (default 64) of the full
-per-timestep hot path -- forward, fp64 softmax + quantiser, range encoder on
-its own CUDA stream, backward + Adam -- replayed from a captured CUDA graph on
-the device-resident stream matrix.  Multi-GPU (torchrun) is weak scaling: every
-rank compresses its own 100 MB shard with its own model; no collective runs in
-the timed region (the max-over-ranks timing reduction happens after it).
+Workload: FADE default model (ModelConfig(): B = 512 streams, 24 M
+parameters, online Adam), one byte per stream per timestep.  At N = 1 it is
+BASELINE.json config 2, a seeded 100 MB enwik8-shaped text stream
+(``corpus.make_text(100_000_000, 12)``); at N > 1 (torchrun) it is config 5,
+a 1 GB text / genome / float32 stream (``corpus.make_modal(10**9, 20)``) cut
+into N contiguous shards, one per GPU, each with its own model and B streams
+(no collective on the hot path).  One bench "step" =
+``--chunk`` timesteps (default 64) of the full per-timestep hot path --
+forward, fp64 softmax + quantiser, range encoder on its own CUDA stream,
+backward + Adam -- replayed from a captured CUDA graph on the device-resident
+stream matrix; per-GPU work per step is fixed, so scaling is weak; the
+max-over-ranks timing reduction happens after the timed region.
 
 Keys beyond the driver contract: ``decompress`` (device decode MB/s through
 fade_decompress on the e2e sample), ``roofline`` (the dominant component, timed
-alone with CUDA events), ``cpu_baseline`` (the CPU oracle port timed on this
-host's cores), ``e2e`` (compress_bytes / decompress_bytes with host buffers),
-``clocks`` (nvidia-smi during the timed region).
+alone with CUDA events), ``cpu_baseline`` (the reference ``dszip`` itself from
+baseline/_ref -- or, if that install is missing, the CPU oracle port -- timed
+on this host's cores), ``e2e`` (compress_bytes / decompress_bytes with host
+buffers; at N > 1 compress_sharded / decompress_sharded with the v2 container
+gather), ``clocks`` (nvidia-smi during the timed region).
 """
 
 from __future__ import annotations
@@ -39,6 +44,9 @@ sys.path.insert(0, ROOT)
 METRIC = "compress/decompress MB/s at 1/2/4/8 B200 at matched bits/byte vs CPU reference"
 UNIT = "MB/s"
 WORKLOAD = "FADE default model (B=512, 24M params, online Adam), 100 MB enwik8-shaped text"
+WORKLOAD_SHARDED = ("FADE default model (B=512 per shard, 24M params each, online Adam), "
+                    "1 GB text/genome/float32 stream in {n} contiguous shards (config 5)")
+MODAL_SIZE, MODAL_SEED = 10 ** 9, 20
 
 
 def parse():
@@ -119,39 +127,80 @@ def peaks():
         return 6650.0, 1590.0 / 2.0, "fallback"
 
 
+def _reference_steps(batch: int, steps: int, warmup: int):
+    """Per-timestep wall times of the reference's own CPU path: ``dszip``
+    installed unmodified in baseline/_ref (pip --target), serial
+    order predict -> quantize -> cum_from_freq -> encode -> train_step
+    (pipeline.py:197-226) on the default config at B streams, on every host
+    core (OpenBLAS threads = nproc, numba kernels).  Falls back to the oracle
+    port (oracle/pipeline.py) if the install is missing.  Returns
+    (seconds per timestep list, kind, description)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    try:
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import dszip  # noqa: F401
+        from dszip.coder import BatchEncoder, cum_from_freq, quantize
+        from dszip.config import ModelConfig as RefConfig
+        from dszip.model import Predictor as RefPredictor
+    except Exception:  # noqa: BLE001 - install absent: the pinned port
+        from oracle.pipeline import time_steps
+        from paper_2604_07239_b200 import ModelConfig
+        t = time_steps(ModelConfig(batch=batch, workers=1), steps=steps, warmup=warmup)
+        return list(t), "port", "oracle port (numpy/OpenBLAS model + C coder)"
+    from paper_2604_07239_b200 import corpus
+    # torchrun exports OMP_NUM_THREADS=1; the reference's BLAS gets every core
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count())
+    except Exception:  # noqa: BLE001 - best effort
+        pass
+    cfg = RefConfig(batch=batch, workers=1)
+    model = RefPredictor(cfg)
+    enc = BatchEncoder(batch)
+    T = cfg.ctx_len
+    n = T + warmup + steps + 1
+    mat = np.frombuffer(corpus.make_text(batch * n, 12), np.uint8).reshape(batch, n)
+    times = []
+    for k in range(warmup + steps):
+        i = T + k
+        t0 = time.perf_counter()
+        probs = model.predict(mat[:, i - T:i])
+        enc.encode(cum_from_freq(quantize(probs)), mat[:, i], step=i)
+        model.train_step(mat[:, i])
+        if k >= warmup:
+            times.append(time.perf_counter() - t0)
+    return times, "reference", f"dszip {dszip.__version__} (baseline/_ref, numba + OpenBLAS)"
+
+
 def cpu_baseline(batch: int, steps: int):
-    """The CPU oracle port (numpy/OpenBLAS model + C coder) on this host."""
-    from oracle.pipeline import time_steps
-    from paper_2604_07239_b200 import ModelConfig
-    cfg = ModelConfig(batch=batch, workers=1)
-    t = time_steps(cfg, steps=steps, warmup=1)
+    """The reference's CPU path on this host (bounded sample of the workload)."""
+    t, kind, what = _reference_steps(batch, steps, 1)
     per = float(np.mean(t))
-    return {"value": batch / per / 1e6, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+    return {"value": batch / per / 1e6, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
             "sample": f"{steps} timesteps (after 1 warm-up) of predict->quantise->encode->train "
-                      f"at B={batch}, default dims, random context; {per:.3f} s/timestep; "
-                      "per-step cost is content-independent (BASELINE.md section 4)"}
+                      f"at B={batch}, default dims, text context; {per:.3f} s/timestep; "
+                      f"{what}; per-step cost is content-independent (BASELINE.md section 4)"}
 
 
 def run_reference(args):
     world, rank, _ = dist_info()
     if rank != 0:
         return
-    from oracle.pipeline import time_steps
-    from paper_2604_07239_b200 import ModelConfig
-    cfg = ModelConfig(batch=args.batch, workers=1)
-    t = time_steps(cfg, steps=args.steps, warmup=args.warmup)
+    t, kind, what = _reference_steps(args.batch, args.steps, args.warmup)
     per = float(np.mean(t))
     value = args.batch / per / 1e6
+    sharded = world > 1
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "step": "1 timestep (B bytes) of the CPU oracle port",
-                   "batch": args.batch},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{args.steps} timesteps after {args.warmup} warm-up, random "
-                                   "context, numpy/OpenBLAS on all host cores"},
+        "config": {"workload": WORKLOAD_SHARDED.format(n=world) if sharded else WORKLOAD,
+                   "step": "1 timestep (B bytes) of the reference CPU path", "batch": args.batch},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                         "sample": f"{args.steps} timesteps after {args.warmup} warm-up, text "
+                                   f"context, {what}, all host cores"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -164,15 +213,32 @@ def run_ours(args):
     from paper_2604_07239_b200.pipeline import StreamPartition
 
     world, rank, local = dist_info()
+    # one process per GPU; a functional dry run with more ranks than GPUs
+    # shares devices round-robin and (NCCL refuses duplicate GPUs) runs the
+    # out-of-timed-region barriers / reductions over gloo
+    ndev = torch.cuda.device_count()
+    local = local % ndev
     torch.cuda.set_device(local)
     pg = None
+    red = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+            red = "cpu"
         pg = dist
     lib = _native.lib()
     cfg = ModelConfig(batch=args.batch, workers=1)
-    data = corpus.make_text(args.size, 12 + rank)
+    if world > 1:
+        # config 5: this rank's contiguous shard of the 1 GB mixed stream
+        from paper_2604_07239_b200.shard import shard_bounds
+        lo, hi = shard_bounds(MODAL_SIZE, world)[rank]
+        data = corpus.make_modal_range(MODAL_SIZE, lo, hi, MODAL_SEED,
+                                       workers=max(1, (os.cpu_count() or 1) // world))
+    else:
+        data = corpus.make_text(args.size, 12)
     part = StreamPartition.from_length(len(data), cfg.batch)
     mat = np.ascontiguousarray(part.split(data))
     L = part.stream_length
@@ -207,7 +273,7 @@ def run_ours(args):
     if pg:
         pg.barrier()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms], dtype=torch.float64, device=red)
     if pg:
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -257,10 +323,8 @@ def run_ours(args):
 
     e2e = None
     dec = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         sample = data[:args.e2e_bytes]
-        if pg:
-            pg.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         blob, res = container.compress_bytes(sample, cfg)
@@ -269,19 +333,52 @@ def run_ours(args):
         back = container.decompress_bytes(blob)
         td = time.perf_counter() - t0
         assert back == sample, "lossless round trip failed"
-        tt = torch.tensor([tc, td], dtype=torch.float64, device="cuda")
-        if pg:
-            pg.all_reduce(tt, op=pg.ReduceOp.MAX)
-        tc, td = float(tt[0]), float(tt[1])
         init_bytes = 4 * (15_484_259 + 16_384 * cfg.batch)
-        e2e = {"value": world * len(sample) / tc / 1e6, "unit": UNIT,
+        e2e = {"value": len(sample) / tc / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": len(sample) + init_bytes,
                "d2h_bytes_per_step": len(blob) + 8 * cfg.batch,
-               "step": f"one compress_bytes() call on a {len(sample)}-byte sample per rank "
-                       "(host input, model init upload, device loop, host container; the "
-                       "seeded numpy parameter draw is cached in-process after its first use)",
+               "step": f"one compress_bytes() call on a {len(sample)}-byte sample (seeded numpy "
+                       "parameter draw, model init upload, host input upload, device loop, "
+                       "bitstream download, host container)",
                "bits_per_byte": 8.0 * len(blob) / len(sample),
-               "decompress_value": world * len(sample) / td / 1e6}
+               "decompress_value": len(sample) / td / 1e6}
+        dec = e2e["decompress_value"]
+    elif not args.no_e2e:
+        # config 5 end to end: every rank compresses its shard of an N x sample
+        # slice of the mixed stream on its own GPU, rank 0 gathers the stream
+        # tables into one v2 container; then the shards decode in parallel and
+        # rank 0 joins and checks the bytes
+        from paper_2604_07239_b200.shard import compress_sharded, decompress_sharded, shard_bounds
+        n = world * args.e2e_bytes
+        lo, hi = shard_bounds(n, world)[rank]
+        mine = corpus.make_modal_range(n, lo, hi, MODAL_SEED, chunk=args.e2e_bytes // 3 + 1)
+        pg.barrier()
+        t0 = time.perf_counter()
+        blob = compress_sharded(mine, cfg, local=True)
+        tc = time.perf_counter() - t0
+        objs = [blob]
+        pg.broadcast_object_list(objs, src=0)
+        pg.barrier()
+        t0 = time.perf_counter()
+        back = decompress_sharded(objs[0])
+        td = time.perf_counter() - t0
+        if rank == 0:
+            assert back == corpus.make_modal_range(n, 0, n, MODAL_SEED,
+                                                   chunk=args.e2e_bytes // 3 + 1), \
+                "sharded lossless round trip failed"
+        tt = torch.tensor([tc, td], dtype=torch.float64, device=red)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        tc, td = float(tt[0]), float(tt[1])
+        init_bytes = 4 * (15_484_259 + 16_384 * cfg.batch)
+        blen = len(objs[0])
+        e2e = {"value": n / tc / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": n + world * init_bytes,
+               "d2h_bytes_per_step": blen,
+               "step": f"compress_sharded() of a {n}-byte mixed sample, {world} shards, one per "
+                       "GPU (parameter draw, uploads, device loop, download, host gather into "
+                       "the v2 container on rank 0); max over ranks",
+               "bits_per_byte": 8.0 * blen / n,
+               "decompress_value": n / td / 1e6}
         dec = e2e["decompress_value"]
 
     base = None
@@ -292,7 +389,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "tf32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "batch": cfg.batch, "timesteps_per_step": S,
+            "config": {"workload": WORKLOAD_SHARDED.format(n=world) if world > 1 else WORKLOAD,
+                       "batch": cfg.batch, "timesteps_per_step": S,
                        "stream_length": L, "parallelism": f"shards{world}",
                        "l2": "working set ~290 MB (params + Adam state) > 126 MB L2; no flush"},
             "decompress": dec, "gpu_launches": launches.value * K * S,

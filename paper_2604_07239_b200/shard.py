@@ -41,8 +41,11 @@ def compress_shard(data: bytes, cfg: ModelConfig, rank: int, world: int, compres
 
 
 def compress_sharded(data: bytes, cfg: ModelConfig, group=None, compress_fn=None,
-                     device: int | None = None, fingerprint_fn=None) -> bytes | None:
-    """Collective entry point: every rank calls it with the same `data`.
+                     device: int | None = None, fingerprint_fn=None,
+                     local: bool = False) -> bytes | None:
+    """Collective entry point: every rank calls it with the same `data`
+    (``local=True``: each rank passes only its own contiguous shard, in rank
+    order, so no rank needs the whole input in memory).
 
     Returns the v2 container on rank 0 and None elsewhere.  Each rank runs
     its shard on ``device`` (default: its own LOCAL_RANK GPU) and stamps it
@@ -53,7 +56,10 @@ def compress_sharded(data: bytes, cfg: ModelConfig, group=None, compress_fn=None
     from . import container
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    res = compress_shard(data, cfg, rank, world, compress_fn, device)
+    if local:
+        res = compress_shard(data, cfg, 0, 1, compress_fn, device)
+    else:
+        res = compress_shard(data, cfg, rank, world, compress_fn, device)
     fp_fn = fingerprint_fn or (lambda c: container.shard_fingerprint(c, res.device or 0))
     # host-side gather of (stream table, bytes) -- the only exchange step
     payload = (res.partition.original_length, res.cfg, [bytes(s) for s in res.streams], res.losses,

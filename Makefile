@@ -9,7 +9,7 @@ SRCS := $(wildcard $(SRC_DIR)/*.cu)
 HDRS := $(wildcard $(SRC_DIR)/*.cuh) include/fade_b200.h
 OBJS := $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
 
-all: $(LIB) oracle
+all: $(LIB) oracle experiments
 
 build/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p build

@@ -108,7 +108,12 @@ struct fade_model {
   uint8_t* ctx_buf = nullptr;   // [B][T]  (predict API)
   uint8_t* tgt_buf = nullptr;   // [B]
   double* loss_buf = nullptr;   // [1]
-  float* cache_snap = nullptr;  // [B][C] for state-free test hooks
+  // cache snapshots (cache [B][C] + ring position): [0] the state before the
+  // last predict (restored when it fails, replayed when a test hook ran in
+  // between), [1] the state around forward_debug / loss_grads
+  float* cache_snap[2] = {};
+  long long* ring_snap[2] = {};
+  uint8_t* live_ctx = nullptr;  // [B][T] context of the pending predict
   float* w12_g = nullptr;
   bool live = false;            // a predict is pending train_step
   int launches_per_step = 0;
@@ -343,6 +348,17 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   // group is a no-op
   const VFlags vf = vflags(M.variant);
   float* h_final = vf.fnr ? a.h : (vf.mixer ? a.h_c : a.h_mix);
+  // the cache operand of the W_mem GEMMs is a ring buffer (allocate: ring_on)
+  // (the forward GEMM runs before mix_fwd counts this step's roll: bias 1)
+  auto ring_operand = [&](GemmDesc& g, int kind) {
+    if (!M.ring_on) return;
+    g.a_ring = kind;
+    g.ring_bias = kind == 1 ? 1 : 0;
+    g.ring_len = C;
+    g.ring_rows = B;
+    g.ring_step = d.D / kBK;
+    g.ring = &m->st->ring;
+  };
   // narrow GEMMs write split-K slices their consumer reduces (plan_splits)
   auto sk = [&](GemmDesc g, int id) {
     g.C = M.sk[id].ws;
@@ -357,6 +373,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
       TRY(bl.add(sk(gd(a.x, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_RPRE)));
     GemmDesc g = gd(a.cache, C, 0, w[P_W_MEM].p, H, 0, B, H, C, EPI_STORE, a.ws_mem, H);
     g.splits = M.splits_mem;
+    ring_operand(g, 1);
     if (vf.global) TRY(bl.add(g));
   }
   if (vf.mixer) {
@@ -450,8 +467,11 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     auto bl = b(G_WROUTE_WMEM);
     if (vf.router)
       TRY(bl.add(adam(gd(a.x, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE])));
-    if (vf.global)
-      TRY(bl.add(adam(gd(a.cache, C, 1, a.dupre, H, 0, C, H, B, EPI_ADAM, nullptr, H), w[P_W_MEM])));
+    if (vf.global) {
+      GemmDesc g = gd(a.cache, C, 1, a.dupre, H, 0, C, H, B, EPI_ADAM, nullptr, H);
+      ring_operand(g, 2);
+      TRY(bl.add(adam(g, w[P_W_MEM])));
+    }
   }
   return FADE_OK;
 }
@@ -502,6 +522,18 @@ static int allocate(fade_model* m) {
   plan_splits(M, {{S_INNER, B, H, X}, {S_CPRE, B, H, H}});
   plan_splits(M, {{S_LOGITS, B, 256, H}});     // head GEMM: -2..5 us (dh split: +1 us)
   M.variant = m->cfg.variant;
+  // the rolling cache as a ring buffer: block writes instead of a (C - D)
+  // float roll per row; needs D and B to be whole numbers of 32-float
+  // k-tiles so the W_mem GEMMs can rotate their TMA coordinates block by
+  // block.  Bit-identical to the roll, but measured slower (B = 512: 341 vs
+  // 335.5 us per timestep, same box; B = 1024 / 4096: neutral): the roll's
+  // rewrite is cheap (2-3 us of trunk_fwd) and the W_mem GEMMs read the ring
+  // operand more slowly (ncu, cold: +1.0 us forward, +3.1 us update), even
+  // block-major and with the old blocks prefetched before the dependency
+  // wait.  Experiments build: FADE_RING=1 turns it on.
+  const bool ring_req = knob("FADE_RING") && atoi(knob("FADE_RING")) != 0;
+  M.ring_on = ring_req && (d.D % kBK == 0) && (d.B % kBK == 0) && vflags(m->cfg.variant).global
+                  ? 1 : 0;
   M.lr = m->cfg.lr;
   M.beta1 = m->cfg.beta1;
   M.beta2 = m->cfg.beta2;
@@ -546,7 +578,11 @@ static int allocate(fade_model* m) {
   items.push_back({(void**)&m->ctx_buf, (size_t)B * d.T});
   items.push_back({(void**)&m->tgt_buf, (size_t)B});
   items.push_back({(void**)&m->loss_buf, sizeof(double) * 4});
-  F(&m->cache_snap, B * C);
+  for (int k = 0; k < 2; ++k) {
+    F(&m->cache_snap[k], B * C);
+    items.push_back({(void**)&m->ring_snap[k], sizeof(long long)});
+  }
+  items.push_back({(void**)&m->live_ctx, (size_t)B * d.T});
 
   size_t total = 0;
   std::vector<size_t> offs;
@@ -760,6 +796,46 @@ static int set_col(fade_model* m, long long col, long long loss_base) {
   return FADE_OK;
 }
 
+// the cache (and its ring position) before a call that must leave no trace:
+// forward_debug, loss_grads, a predict that fails
+static int snapshot_cache(fade_model* m, int k) {
+  const size_t cbytes = sizeof(float) * m->d.B * m->d.C;
+  CK(cudaMemcpyAsync(m->cache_snap[k], m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  CK(cudaMemcpyAsync(m->ring_snap[k], &m->st->ring, sizeof(long long), cudaMemcpyDeviceToDevice,
+                     m->s_main));
+  return FADE_OK;
+}
+static int restore_cache(fade_model* m, int k) {
+  const size_t cbytes = sizeof(float) * m->d.B * m->d.C;
+  CK(cudaMemcpyAsync(m->M.a.cache, m->cache_snap[k], cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  CK(cudaMemcpyAsync(&m->st->ring, m->ring_snap[k], sizeof(long long), cudaMemcpyDeviceToDevice,
+                     m->s_main));
+  return FADE_OK;
+}
+// the Predictor API's step input: the context uploaded to ctx_buf
+static StepIO api_io(fade_model* m) {
+  StepIO io{};
+  io.src = m->ctx_buf;
+  io.ld_src = m->d.T;
+  io.use_col = 0;
+  return io;
+}
+// A test hook (forward_debug, loss_grads) ran between predict and
+// train_step and overwrote the saved activations; the reference keeps its
+// live graph (model.py:195-200, 217-237).  Re-run the pending predict from
+// its saved state: same inputs, same kernels, so the activations are
+// bit-identical to the original ones.
+static int replay_live(fade_model* m) {
+  if (!m->live) return FADE_OK;
+  TRY(restore_cache(m, 0));
+  CK(cudaMemcpyAsync(m->ctx_buf, m->live_ctx, (size_t)m->d.B * m->d.T, cudaMemcpyDeviceToDevice,
+                     m->s_main));
+  StepIO io = api_io(m);
+  io.head.want_probs = 1;
+  TRY(forward(m, io, true));
+  return FADE_OK;
+}
+
 // runs a callable when the scope exits (every error path included)
 template <class F>
 struct Defer {
@@ -935,16 +1011,56 @@ int fade_model_get_tensor(fade_model_t* m, int kind, int index, float* host, int
   return FADE_OK;
 }
 
+// The cache crosses the ABI in the reference's logical order ([B][C], oldest
+// block first, model.py:125-127); on the device it may be the block-major ring
+// (ModelPtrs.ring_on): logical column c of stream b at
+// [((c/32 + shift) mod C/32) * B + b] * 32 + c mod 32.
+static float* ring_block(const Dims& d, float* ring, int shift, int b, int j) {
+  return ring + (((size_t)((j + shift) % (d.C / 32)) * d.B + b) << 5);
+}
+static void logical_to_ring(const Dims& d, const float* logical, float* ring) {
+  for (int b = 0; b < d.B; ++b)
+    for (int j = 0; j < d.C / 32; ++j)
+      memcpy(ring_block(d, ring, 0, b, j), logical + (size_t)b * d.C + 32 * j, 32 * sizeof(float));
+}
+static void ring_to_logical(const Dims& d, float* ring, int shift, float* logical) {
+  for (int b = 0; b < d.B; ++b)
+    for (int j = 0; j < d.C / 32; ++j)
+      memcpy(logical + (size_t)b * d.C + 32 * j, ring_block(d, ring, shift, b, j), 32 * sizeof(float));
+}
+
 int fade_model_set_cache(fade_model_t* m, const float* host) {
   ON_DEVICE(m->device);
-  CK(cudaMemcpy(m->M.a.cache, host, sizeof(float) * m->d.B * m->d.C, cudaMemcpyHostToDevice));
+  CK(cudaDeviceSynchronize());
+  const Dims& d = m->d;
+  const size_t n = (size_t)d.B * d.C;
+  if (m->M.ring_on) {
+    std::vector<float> tmp(n);
+    logical_to_ring(d, host, tmp.data());
+    CK(cudaMemcpy(m->M.a.cache, tmp.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMemcpy(m->M.a.cache, host, sizeof(float) * n, cudaMemcpyHostToDevice));
+  }
+  const long long zero = 0;
+  CK(cudaMemcpy(&m->st->ring, &zero, sizeof(long long), cudaMemcpyHostToDevice));
   return FADE_OK;
 }
 
 int fade_model_get_cache(fade_model_t* m, float* host) {
   ON_DEVICE(m->device);
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(host, m->M.a.cache, sizeof(float) * m->d.B * m->d.C, cudaMemcpyDeviceToHost));
+  const Dims& d = m->d;
+  const size_t n = (size_t)d.B * d.C;
+  if (!m->M.ring_on) {
+    CK(cudaMemcpy(host, m->M.a.cache, sizeof(float) * n, cudaMemcpyDeviceToHost));
+    return FADE_OK;
+  }
+  long long r = 0;
+  CK(cudaMemcpy(&r, &m->st->ring, sizeof(long long), cudaMemcpyDeviceToHost));
+  const int nb = d.C / 32;
+  std::vector<float> tmp(n);
+  CK(cudaMemcpy(tmp.data(), m->M.a.cache, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  ring_to_logical(d, tmp.data(), (int)((r * (d.D / 32)) % nb), host);
   return FADE_OK;
 }
 
@@ -967,13 +1083,6 @@ int fade_model_get_counters(fade_model_t* m, int64_t* adam_t, int64_t* step_coun
   return FADE_OK;
 }
 
-static StepIO api_io(fade_model_t* m) {
-  StepIO io{};
-  io.src = m->ctx_buf;
-  io.ld_src = m->d.T;
-  io.use_col = 0;
-  return io;
-}
 
 int fade_model_predict(fade_model_t* m, const uint8_t* ctx, double* probs, double* alpha,
                        fade_error_t* err) {
@@ -985,15 +1094,18 @@ int fade_model_predict(fade_model_t* m, const uint8_t* ctx, double* probs, doubl
   // the trunk kernel rolls the cache in place before the head can find a
   // non-finite logit; the reference commits the cache only after its finite
   // check (model.py:190-196), so a failed predict restores the snapshot
-  const size_t cbytes = sizeof(float) * d.B * d.C;
-  CK(cudaMemcpyAsync(m->cache_snap, m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  TRY(snapshot_cache(m, 0));
   CK(cudaMemcpyAsync(m->ctx_buf, ctx, (size_t)d.B * d.T, cudaMemcpyHostToDevice, m->s_main));
+  CK(cudaMemcpyAsync(m->live_ctx, m->ctx_buf, (size_t)d.B * d.T, cudaMemcpyDeviceToDevice,
+                     m->s_main));
   StepIO io = api_io(m);
   io.head.want_probs = 1;
   TRY(forward(m, io, true));
   CK(cudaStreamSynchronize(m->s_main));
   if (int st = check_error(m, err)) {
-    CK(cudaMemcpy(m->M.a.cache, m->cache_snap, cbytes, cudaMemcpyDeviceToDevice));
+    m->live = false;
+    TRY(restore_cache(m, 0));
+    CK(cudaStreamSynchronize(m->s_main));
     return st;
   }
   if (probs)
@@ -1062,14 +1174,14 @@ int fade_model_forward_debug(fade_model_t* m, const uint8_t* ctx, const char* pa
     return FADE_ERR_USAGE;
   }
   const Dims& d = m->d;
-  const size_t cbytes = sizeof(float) * d.B * d.C;
-  CK(cudaMemcpyAsync(m->cache_snap, m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  TRY(snapshot_cache(m, 1));
   CK(cudaMemcpyAsync(m->ctx_buf, ctx, (size_t)d.B * d.T, cudaMemcpyHostToDevice, m->s_main));
   StepIO io = api_io(m);
   // (the head kernel reduces the logits' split-K slices into a.logits)
   TRY(forward(m, io, true));
   CK(cudaMemcpyAsync(out, src, sizeof(float) * d.B * width, cudaMemcpyDeviceToHost, m->s_main));
-  CK(cudaMemcpyAsync(m->M.a.cache, m->cache_snap, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  TRY(restore_cache(m, 1));
+  TRY(replay_live(m));
   CK(cudaStreamSynchronize(m->s_main));
   return FADE_OK;
 }
@@ -1077,8 +1189,7 @@ int fade_model_forward_debug(fade_model_t* m, const uint8_t* ctx, const char* pa
 int fade_model_loss_grads(fade_model_t* m, const uint8_t* ctx, const uint8_t* targets, double* loss) {
   ON_DEVICE(m->device);
   const Dims& d = m->d;
-  const size_t cbytes = sizeof(float) * d.B * d.C;
-  CK(cudaMemcpyAsync(m->cache_snap, m->M.a.cache, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  TRY(snapshot_cache(m, 1));
   CK(cudaMemcpyAsync(m->ctx_buf, ctx, (size_t)d.B * d.T, cudaMemcpyHostToDevice, m->s_main));
   CK(cudaMemcpyAsync(m->tgt_buf, targets, (size_t)d.B, cudaMemcpyHostToDevice, m->s_main));
   int64_t sc = 0, t = 0;
@@ -1090,7 +1201,8 @@ int fade_model_loss_grads(fade_model_t* m, const uint8_t* ctx, const uint8_t* ta
   io.head.ld_tgt = 1;
   TRY(forward(m, io, true));
   TRY(backward(m, io, true, m->loss_buf, 0));
-  CK(cudaMemcpyAsync(m->M.a.cache, m->cache_snap, cbytes, cudaMemcpyDeviceToDevice, m->s_main));
+  TRY(restore_cache(m, 1));
+  TRY(replay_live(m));
   CK(cudaStreamSynchronize(m->s_main));
   TRY(check_error(m, nullptr));
   CK(cudaMemcpy(loss, m->loss_buf, sizeof(double), cudaMemcpyDeviceToHost));

@@ -94,8 +94,20 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   int s;
   // a CTA pair splits the B tile: each CTA stages BN/2 columns
   const int pair = d.pair == 2 ? 2 : 1;
-  if (!P->a_mn) s = make_tmap_kmajor(&P->ta, d.A, d.M, d.K, d.lda, kBM);
-  else s = make_tmap_mnmajor(&P->ta, d.A, d.M, d.K, d.lda);
+  if (d.a_ring) {
+    // block-major ring [ring_len/32][ring_rows][32]: a 2-D view of 32-wide rows
+    const long long rows = (long long)(d.ring_len / kBK) * d.ring_rows;
+    if (d.ring_len % kBK || !d.ring || d.ring_rows % kBK || d.ring_step < 1) {
+      set_last_error("ring-buffer operand: extent and rows must be 32-multiples");
+      return FADE_ERR_USAGE;
+    }
+    s = !P->a_mn ? make_tmap_kmajor(&P->ta, d.A, rows, kBK, kBK, kBM)
+                 : make_tmap_mnmajor(&P->ta, d.A, kBK, rows, kBK);
+  } else if (!P->a_mn) {
+    s = make_tmap_kmajor(&P->ta, d.A, d.M, d.K, d.lda, kBM);
+  } else {
+    s = make_tmap_mnmajor(&P->ta, d.A, d.M, d.K, d.lda);
+  }
   if (s) return s;
   if (!P->b_mn) s = make_tmap_kmajor(&P->tb, d.B, d.N, d.K, d.ldb, BN / pair);
   else s = make_tmap_mnmajor(&P->tb, d.B, d.N, d.K, d.ldb);
@@ -108,6 +120,12 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   P->tiles_n = cdiv(d.N, BN);
   P->epi = d.epi;
   P->bias = d.bias;
+  P->a_ring = d.a_ring;
+  P->ring_len = d.ring_len;
+  P->ring_rows = d.ring_rows;
+  P->ring_step = d.ring_step;
+  P->ring_bias = d.ring_bias;
+  P->ring = d.ring;
   if (P->splits > 1 && d.epi != EPI_STORE) {
     set_last_error("split-K is only valid with the partial-store epilogue");
     return FADE_ERR_USAGE;
@@ -142,20 +160,35 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   return s;
 }
 
-template <int BN, int ET, int OCC = 1, int PAIR = 1>
-static int launch_cfg(GemmParams& G, cudaStream_t st) {
+template <int BN, int ET, int OCC, int PAIR, bool RING>
+static int launch_inst(GemmParams& G, cudaStream_t st) {
   using Cfg = GemmCfg<BN, ET, OCC, PAIR>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN, ET, OCC, PAIR>,
+    attr_err = cudaFuncSetAttribute(k_gemm_tf32<BN, ET, OCC, PAIR, RING>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
   });
   FADE_CUDA_TRY(attr_err);
-  FADE_CUDA_TRY(launch_pdl_cluster(k_gemm_tf32<BN, ET, OCC, PAIR>, dim3(G.total_tiles * PAIR),
+  FADE_CUDA_TRY(launch_pdl_cluster(k_gemm_tf32<BN, ET, OCC, PAIR, RING>, dim3(G.total_tiles * PAIR),
                                    dim3(kGemmThreads), (size_t)Cfg::kSmem, st, PAIR, G));
   FADE_CUDA_TRY(cudaGetLastError());
   return FADE_OK;
+}
+
+// ring-buffer operands exist only for the single-CTA, stage-aliased
+// configurations the W_mem GEMMs use
+template <int BN, int ET, int OCC = 1, int PAIR = 1>
+static int launch_cfg(GemmParams& G, cudaStream_t st) {
+  bool ring = false;
+  for (int q = 0; q < G.nprob; ++q) ring = ring || G.prob[q].a_ring;
+  if (!ring) return launch_inst<BN, ET, OCC, PAIR, false>(G, st);
+  if constexpr (PAIR == 1 && ET == 0) {
+    return launch_inst<BN, ET, OCC, PAIR, true>(G, st);
+  } else {
+    set_last_error("ring-buffer operand in an unsupported GEMM configuration");
+    return FADE_ERR_USAGE;
+  }
 }
 
 template <int BN, int PAIR>
@@ -197,9 +230,9 @@ int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   }
   G.total_tiles = t;
   if (t == 0) return FADE_OK;
-  if (G.ws) {   // persistent: STORE / GEGLU epilogues only
+  if (G.ws) {   // persistent: STORE / GEGLU epilogues only, no ring operands
     for (int q = 0; q < G.nprob; ++q)
-      if (G.prob[q].epi != EPI_STORE && G.prob[q].epi != EPI_GEGLU) {
+      if ((G.prob[q].epi != EPI_STORE && G.prob[q].epi != EPI_GEGLU) || G.prob[q].a_ring) {
         set_last_error("the persistent GEMM runs only the store and GeGLU epilogues");
         return FADE_ERR_USAGE;
       }

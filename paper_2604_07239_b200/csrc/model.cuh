@@ -73,12 +73,19 @@ struct StepState {   // device-resident, so one captured graph replays every ste
   AdamScalars adam;
   unsigned long long err_key;   // min over (step << 24 | stream << 3 | code); ~0 = none
   double alpha_sum, alpha_min, alpha_max;   // last predict's router stats
+  // ring-buffer cache (ModelPtrs.ring_on): rolls counted since the cache was
+  // last set; logical D-block j of every cache row lives at physical D-block
+  // (j + ring) mod (C / D).  trunk_fwd writes the new block at D-block
+  // `ring`, the forward W_mem GEMM reads with ring + 1 (ring_bias), and
+  // mix_fwd (the next kernel) counts the roll.
+  long long ring;
 };
 
 struct Acts {        // saved activations and gradient scratch, all [B][ld]
   // forward
   float *x, *x_hat, *x_inv, *gpre, *vpre, *loc, *loc_hat, *loc_inv, *conv_pre, *h_l;
-  float *cache;                 // [B][C] rolling cache (rolled in place each predict)
+  float *cache;                 // [B][C] rolling cache (ring buffer when ring_on, else rolled
+                                //  in place each predict)
   float *ws_mem, *upre, *h_g, *alpha, *h_mix, *z_hat, *z_inv, *z;   // router pre-activation: sk[S_RPRE]
   float *zd, *u, *inner, *gate, *h_c, *z2_hat, *z2_inv, *z2;
   float *a12, *wide, *ws_f, *n_hat, *n_inv, *nrm, *h, *logits;
@@ -117,6 +124,12 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   // executors only: device event tape [steps][kTapeSlots] indexed by
   // col - loss_base (null: not recorded)
   unsigned long long* tape;
+  // 1: the rolling cache is a ring buffer (D and B multiples of the 32-float
+  // GEMM k-tile): predict writes one block in place instead of moving (C - D)
+  // floats per row (ref nn/ops.py:219-231 roll_cache semantics unchanged).
+  // Layout then block-major, cache[(kb * B + b) * 32 + e] for physical
+  // 32-column block kb, so the W_mem GEMMs read whole contiguous tiles.
+  int ring_on;
 };
 __device__ __forceinline__ unsigned long long* tape_at(const ModelPtrs& M, int slot) {
   return M.tape + kTapeSlots * (M.st->col - M.st->loss_base) + slot;

@@ -150,10 +150,20 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   if (M.tape && b == 0 && tid == 0) *tape_at(M, 0) = gtimer_ns();
   float* crow = M.a.cache + (long long)b * d.C;
   const int n4 = (d.C - d.D) / 4;        // float4 count the roll moves
+  // ring buffer (block-major [C/32][B][32], model.cuh): the new block
+  // overwrites the oldest one in place; nothing else moves (ref
+  // ops.py:219-231 semantics).  Element o of the new block lands at
+  // ring_elem(o); without the ring, at crow[C - D + o] after the roll.
+  const bool ring = M.ring_on;
+  const int rnb = d.C / 32, rstep = d.D / 32;
+  const int rb0 = ring ? (int)((M.st->ring * rstep) % rnb) : 0;
+  auto ring_elem = [&](int o) -> float* {
+    return M.a.cache + (((long long)((rb0 + (o >> 5)) % rnb) * d.B + b) << 5) + (o & 31);
+  };
   if constexpr (DT > 0) {
     // the roll's reads depend on nothing this kernel computes: start them
     // first (cp.async into smem) so they land under the LayerNorm/GeGLU work
-    if (vf.global) {
+    if (vf.global && !ring) {
       for (int q = tid; q < n4; q += blockDim.x)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(cstage + 4 * q)),
@@ -242,9 +252,10 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
         }
         M.a.gpre[(long long)b * DT + tid] = gs;
         M.a.vpre[(long long)b * DT + tid] = vs;
-        crow[d.C - DT + tid] = gelu_f(gs) * vs;
+        *(ring ? ring_elem(tid) : crow + d.C - DT + tid) = gelu_f(gs) * vs;
       }
-      for (int q = tid; q < n4; q += blockDim.x) *(float4*)(crow + 4 * q) = *(const float4*)(cstage + 4 * q);
+      if (!ring)
+        for (int q = tid; q < n4; q += blockDim.x) *(float4*)(crow + 4 * q) = *(const float4*)(cstage + 4 * q);
       __syncthreads();     // locs partials consumed
     }
   } else if (vf.global) {
@@ -259,7 +270,10 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     blk[o] = gelu_f(g) * v;
   }
   // roll the cache in place: new[j] = old[j + D]; new[C-D+o] = block[o]
-  {
+  if (ring) {
+    __syncthreads();
+    for (int o = tid; o < d.D; o += blockDim.x) *ring_elem(o) = blk[o];
+  } else {
     constexpr int U = 4;
     for (int base = 0; base < n4; base += U * (int)blockDim.x) {
       float4 r[U];
@@ -382,7 +396,8 @@ void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
   const Dims& d = M.d;
   const size_t smem = sizeof(float) * (3 * d.H + (2 + d.K) * d.D * d.D + d.D + 2 * d.T + 32) +
                       sizeof(int) * d.T;
-  const size_t smem_dt = smem + 16 + sizeof(float) * (d.C - d.D);   // + the staged cache tail
+  // + the staged cache tail when the cache rolls (a ring buffer moves nothing)
+  const size_t smem_dt = smem + 16 + (M.ring_on ? 0 : sizeof(float) * (d.C - d.D));
   if (d.D == 32 && d.T == 16 && d.K == 3 && smem_dt <= 56 * 1024) {
     static const cudaError_t attr = cudaFuncSetAttribute(
         k_trunk_fwd<32, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 1024);
@@ -409,6 +424,10 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
   const long long plane = (long long)d.B * d.H;
   const float lam = M.w[P_LAM_MEM].p[0];
   const VFlags vf = vflags(M.variant);
+  // count this step's roll of the ring-buffer cache: trunk_fwd wrote the new
+  // block at the old position and the forward W_mem GEMM (ring_bias 1) has
+  // read; no other kernel of this grid reads the position
+  if (M.ring_on && b == 0 && tid == 0) M.st->ring += 1;
   if (vf.global) split_row(ups, part, M.a.ws_mem, plane, rH, d.H, M.splits_mem);
   float asum = 0.f, amin = 3.4e38f, amax = -3.4e38f;
   for (int j = tid; j < d.H; j += blockDim.x) {

@@ -206,3 +206,69 @@ def test_event_tape_orders_the_pingpong_protocol():
         assert tr == cyc * (len(tr) // 4)
     el = [r["elapsed_s"] for r in res.metrics]
     assert all(b > a for a, b in zip(el, el[1:])) and el[0] > 0
+
+
+RING_CHECK = """
+import sys
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+import test_gpu_default_and_errors as t
+t._ring_check()
+print("RING_OK")
+"""
+
+
+def test_ring_buffer_cache_tracks_the_oracle_roll():
+    """The ring-buffer cache (experiments build, FADE_RING=1; off in the
+    shipped library, engine.cu: measured slower) against the oracle's roll."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    lib = os.path.join(ROOT, "build", "exp", "libfade_b200.so")
+    if not os.path.exists(lib):
+        pytest.skip("experiments build (make experiments) not present")
+    env = dict(os.environ, FADE_LIB_PATH=lib, FADE_RING="1")
+    code = RING_CHECK.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert "RING_OK" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
+
+
+def test_roll_cache_tracks_the_oracle_roll():
+    """The shipped roll: same checks as the ring variant."""
+    _ring_check()
+
+
+def _ring_check():
+    """D = 32, B = 64 runs the rolling cache as a block-major ring buffer (one
+    block written per predict, the W_mem GEMMs rotate their TMA coordinates).  Over 20 steps
+    (the 8-block ring wraps twice) the logical cache the device reports, the
+    probabilities and the losses follow the CPU oracle's explicit roll
+    (ref nn/ops.py:219-231); forward_debug and a failed predict leave the
+    ring position untouched."""
+    from oracle.model import OracleModel
+    from paper_2604_07239_b200 import ModelConfig, corpus
+    from paper_2604_07239_b200.model import Predictor
+    cfg = ModelConfig(ctx_len=4, embed_dim=32, cache_dim=256, mix_dim=32, expand_dim=256,
+                      batch=64, workers=1, seed=4)
+    L = 30
+    mat = np.frombuffer(corpus.make_text(cfg.batch * L, 5), np.uint8).reshape(cfg.batch, L)
+    m, o = Predictor(cfg), OracleModel(cfg)
+    T = cfg.ctx_len
+    for i in range(T, T + 20):
+        p = m.predict(mat[:, i - T:i])
+        q = o.predict(mat[:, i - T:i])
+        assert np.abs(p - q).max() < 2e-2, i
+        if i == T + 9:
+            before = m.save_state()["cache"]
+            m.forward_debug(mat[:, i - T + 1:i + 1])
+            np.testing.assert_array_equal(m.save_state()["cache"], before)
+        np.testing.assert_allclose(m.save_state()["cache"], o.cache, atol=2e-2)
+        lg, lr = m.train_step(mat[:, i]), o.train_step(mat[:, i])
+        assert abs(lg - lr) < 2e-2, i
+    # a cache set through the ABI reads back unchanged (ring reset to 0)
+    st = m.save_state()
+    st["cache"] = np.arange(cfg.batch * cfg.cache_dim, dtype=np.float32).reshape(cfg.batch, -1)
+    m.load_state(st)
+    np.testing.assert_array_equal(m.save_state()["cache"], st["cache"])

@@ -626,15 +626,21 @@ struct StepIO {
 
 // L2 persistence for the per-stream W_U values (33.5 MB at B = 512, read by
 // bmm_fwd and read-modify-written by bmm_bwd every step) in the persisting L2
-// carve-out: -3 us per step.  Pinning p and m (67 MB) measured +32 us (the
-// carve-out starves the other kernels' L2).  FADE_L2PIN=0/1/2 overrides.
-static int l2_pin_mode() {
-  static const int mode = knob("FADE_L2PIN") ? atoi(knob("FADE_L2PIN")) : 1;
-  return mode;
+// carve-out: -3 us per step at B = 256 / 512.  It only pays while W_U is a
+// small part of the 126 MB L2: at B = 1024 (67 MB) the step takes 600 instead
+// of 532 us and at B = 4096 (268 MB) 2.30 instead of 1.61 ms (the carve-out
+// starves every other kernel's L2; bmm_bwd alone runs at 2.7 instead of
+// 6.2 TB/s).  Pinning p and m (67 MB) measured +32 us at B = 512.
+// Experiments build: FADE_L2PIN=0/1/2 overrides.
+constexpr size_t kL2PinMaxBytes = 48ull << 20;
+static int l2_pin_mode(const Dims& d) {
+  static const int forced = knob("FADE_L2PIN") ? atoi(knob("FADE_L2PIN")) : -1;
+  if (forced >= 0) return forced;
+  return sizeof(float) * (size_t)d.B * d.X * d.X <= kL2PinMaxBytes ? 1 : 0;
 }
 struct L2Pin {
   explicit L2Pin(const fade_model* m) {
-    const int mode = l2_pin_mode();
+    const int mode = l2_pin_mode(m->d);
     if (!mode) return;
     const Tensor4& t = m->M.w[P_W_MIX];
     const size_t n = sizeof(float) * (size_t)m->d.B * m->d.X * m->d.X;
@@ -921,8 +927,8 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   CK(cudaEventCreateWithFlags(&m->ev_side_done, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&m->ev_coder_join, cudaEventDisableTiming));
   TRY(allocate(m.get()));
-  if (l2_pin_mode()) {
-    const size_t want = sizeof(float) * (size_t)d.B * d.X * d.X * (l2_pin_mode() == 2 ? 2 : 1);
+  if (l2_pin_mode(d)) {
+    const size_t want = sizeof(float) * (size_t)d.B * d.X * d.X * (l2_pin_mode(d) == 2 ? 2 : 1);
     int maxp = 0, maxw = 0;
     CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device));
     CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, device));
@@ -941,6 +947,12 @@ int fade_model_destroy(fade_model_t* m) {
   DeviceScope dscope(m->device);
   cudaDeviceSynchronize();
   if (m->bench_exec) cudaGraphExecDestroy(m->bench_exec);
+  if (m->l2_persist) {
+    // give the persisting carve-out back: a later, larger model (whose W_U
+    // does not fit) must not run with part of L2 set aside
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
   dev_free(m->mem, m->s_main);
   cudaStreamSynchronize(m->s_main);
   for (auto& e : m->ev) cudaEventDestroy(e);

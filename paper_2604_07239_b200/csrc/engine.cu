@@ -157,6 +157,9 @@ static SmallLayout make_small_layout(const Dims& d) {
   s.conv_k = o; o += d.K * d.D * d.D;
   s.w_gate = o; o += d.D * d.D;  s.w_val = o; o += d.D * d.D;
   s.lam_out = o++; s.lam_mix = o++; s.lam_mem = o++;
+  // rowred rows start 16-byte aligned (the warp-per-row kernels store float4s);
+  // the 0-3 padding slots stay zero: zero gradient, Adam leaves them at 0
+  o = (o + 3) / 4 * 4;
   s.rowred = o;
   s.b_head = o; o += 256;
   s.total = o;
@@ -295,9 +298,10 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   m->bn[G_DWIDE] = kWideBN;
   // the big Adam GEMMs: 128-wide tiles at two CTAs per SM, so one CTA's
   // streamed Adam epilogue overlaps the other's mainloop
+  static const long occ1_ids = knob("FADE_OCC1") ? atol(knob("FADE_OCC1")) : 0;   // experiments
   for (int id : {G_W12, G_WF, G_WROUTE_WMEM}) {
     m->bn[id] = 128;
-    Gs[id].occ = 2;
+    Gs[id].occ = ((occ1_ids >> id) & 1) ? 1 : 2;
   }
   // the backward's narrow GEMMs at half the shared memory (4-stage ring,
   // ~97 KB instead of 8 stages / ~193 KB, or 5 stages + 3 dedicated Adam

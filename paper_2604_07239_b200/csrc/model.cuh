@@ -135,6 +135,15 @@ __device__ __forceinline__ unsigned long long* tape_at(const ModelPtrs& M, int s
   return M.tape + kTapeSlots * (M.st->col - M.st->loss_base) + slot;
 }
 
+// warp-per-row variants (row_warp.cu); false: geometry not covered (H % 128)
+bool launch_mix_fwd_w(const ModelPtrs& M, cudaStream_t s);
+bool launch_coarse_fwd_w(const ModelPtrs& M, cudaStream_t s);
+bool launch_out_fwd_w(const ModelPtrs& M, cudaStream_t s);
+bool launch_out_bwd_w(const ModelPtrs& M, cudaStream_t s);
+bool launch_coarse_bwd_w(const ModelPtrs& M, cudaStream_t s);
+bool launch_mix_bwd_w(const ModelPtrs& M, cudaStream_t s);
+bool row_warp_enabled(int B);
+
 // row kernels (model_kernels.cu)
 void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s);

@@ -9,6 +9,17 @@
 
 namespace fade {
 
+// warp-per-row kernels (row_warp.cu) for H % 128 == 0; experiments build:
+// FADE_ROW_WARP=0 keeps the CTA-per-row kernels below
+// Measured per B (timestep, same box): B = 512 336 -> 364 us, 1024 530 ->
+// 547 us (one warp per row is too little parallelism per row when the grid is
+// small), 2048 883 -> 844 us, 4096 1631 -> 1547 us; so B >= 2048 only.
+bool row_warp_enabled(int B) {
+  static const int forced = knob("FADE_ROW_WARP") ? atoi(knob("FADE_ROW_WARP")) : -1;
+  if (forced >= 0) return forced != 0;
+  return B >= 2048;
+}
+
 constexpr int kRowMax = 512;
 constexpr int kBmmThreads = 128;
 constexpr int kBmmRows = 16;      // W_U rows per k_bmm_bwd CTA (its 25 KB of smem fits beside
@@ -481,6 +492,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
 }
 
 void launch_mix_fwd(const ModelPtrs& M, cudaStream_t s) {
+  if (row_warp_enabled(M.d.B) && launch_mix_fwd_w(M, s)) return;
   launch_pdl(k_mix_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (6 * M.d.H + 32), s,
              M);
 }
@@ -572,6 +584,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_fwd(ModelPtrs M) {
 }
 
 void launch_coarse_fwd(const ModelPtrs& M, cudaStream_t s) {
+  if (row_warp_enabled(M.d.B) && launch_coarse_fwd_w(M, s)) return;
   launch_pdl(k_coarse_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
@@ -603,6 +616,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_out_fwd(ModelPtrs M) {
 }
 
 void launch_out_fwd(const ModelPtrs& M, cudaStream_t s) {
+  if (row_warp_enabled(M.d.B) && launch_out_fwd_w(M, s)) return;
   launch_pdl(k_out_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (5 * M.d.H + 32), s,
              M);
 }
@@ -866,6 +880,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_out_bwd(ModelPtrs M) {
 }
 
 void launch_out_bwd(const ModelPtrs& M, cudaStream_t s) {
+  if (row_warp_enabled(M.d.B) && launch_out_bwd_w(M, s)) return;
   launch_pdl(k_out_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
@@ -910,6 +925,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_bwd(ModelPtrs M) {
 }
 
 void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s) {
+  if (row_warp_enabled(M.d.B) && launch_coarse_bwd_w(M, s)) return;
   launch_pdl(k_coarse_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (5 * M.d.H + 32),
              s, M);
 }
@@ -1182,6 +1198,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_bwd(ModelPtrs M) {
 }
 
 void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s) {
+  if (row_warp_enabled(M.d.B) && launch_mix_bwd_w(M, s)) return;
   launch_pdl(k_mix_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 

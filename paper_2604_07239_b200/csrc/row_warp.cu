@@ -1,0 +1,457 @@
+// Warp-per-row variants of the hidden-width row kernels (H a multiple of 128,
+// H <= 1024 -- the default H = 512 and the mid test geometry H = 128).
+//
+// One warp owns one stream row: lane l holds columns 4l + 128k (k < NV = H/128)
+// as float4s, so every global access of the row is one coalesced 512-byte
+// transaction per k, all of a row's loads are in flight together, and the
+// LayerNorm / residual reductions are warp butterflies -- no __syncthreads and
+// no shared memory.  A CTA carries kRowWarps rows.  Against one 512-thread CTA
+// per row this removes the barrier-separated phases that made every row a
+// chain of dependent round trips (B = 4096: mix_fwd 87 us, coarse_bwd 129 us
+// in the step graph).
+//
+// Semantics are those of the CTA-per-row kernels in model_kernels.cu
+// (model.py:128-172 and their backward); only the summation order of the
+// fixed-order reductions differs (lane partials, then the butterfly), and it
+// is the same for the encoder and the decoder.
+#include "model.cuh"
+
+namespace fade {
+
+constexpr int kRowWarps = 4;
+
+template <int NV>
+struct RowV {
+  float4 v[NV];
+};
+
+template <int NV>
+__device__ __forceinline__ RowV<NV> ld_row(const float* __restrict__ row) {
+  const int lane = threadIdx.x & 31;
+  RowV<NV> r;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) r.v[k] = *(const float4*)(row + 4 * lane + 128 * k);
+  return r;
+}
+template <int NV>
+__device__ __forceinline__ void st_row(float* __restrict__ row, const RowV<NV>& r) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) *(float4*)(row + 4 * lane + 128 * k) = r.v[k];
+}
+// element e (0..3) of float4 k
+__device__ __forceinline__ float& el(float4& f, int e) {
+  return e == 0 ? f.x : (e == 1 ? f.y : (e == 2 ? f.z : f.w));
+}
+__device__ __forceinline__ float el(const float4& f, int e) {
+  return e == 0 ? f.x : (e == 1 ? f.y : (e == 2 ? f.z : f.w));
+}
+template <int NV>
+__device__ __forceinline__ float row_sum(const RowV<NV>& r) {
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) s += (r.v[k].x + r.v[k].y) + (r.v[k].z + r.v[k].w);
+  return warp_sum(s);
+}
+// Split-K planes of a [B][H] GEMM output reduced in plane order into four
+// interleaved accumulators (the split_sum order), row `row`.
+template <int NV>
+__device__ __forceinline__ RowV<NV> ld_split(const float* __restrict__ ws, long long plane,
+                                             long long rowoff, int S) {
+  const int lane = threadIdx.x & 31;
+  RowV<NV> out;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    float4 a[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) a[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* p = ws + rowoff + 4 * lane + 128 * k;
+#pragma unroll 4
+    for (int s = 0; s < S; ++s) {
+      const float4 v = *(const float4*)(p + s * plane);
+      float4& t = a[s & 3];
+      t.x += v.x;
+      t.y += v.y;
+      t.z += v.z;
+      t.w += v.w;
+    }
+    out.v[k] = make_float4((a[0].x + a[1].x) + (a[2].x + a[3].x), (a[0].y + a[1].y) + (a[2].y + a[3].y),
+                           (a[0].z + a[1].z) + (a[2].z + a[3].z), (a[0].w + a[1].w) + (a[2].w + a[3].w));
+  }
+  return out;
+}
+// LayerNorm statistics (ops.py:94-101): mean, then mean of squared deviations
+template <int NV>
+__device__ __forceinline__ void row_ln_stats(const RowV<NV>& x, float n, float* mu, float* inv) {
+  const float m = row_sum(x) / n;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float c = el(x.v[k], e) - m;
+      q += c * c;
+    }
+  const float var = warp_sum(q) / n;
+  *mu = m;
+  *inv = __fdiv_rn(1.0f, __fsqrt_rn(var + kLnEps));
+}
+
+#define ROW_PROLOGUE                                                   \
+  pdl_enter();                                                         \
+  const int lane = threadIdx.x & 31;                                   \
+  const int b = blockIdx.x * kRowWarps + (threadIdx.x >> 5);           \
+  if (b >= M.d.B) return;                                              \
+  const int H = NV * 128;                                              \
+  const long long rH = (long long)b * H;                               \
+  const long long plane = (long long)M.d.B * H;                        \
+  (void)plane;                                                         \
+  (void)lane;
+
+// ---------------------------------------------------------------------------
+// forward
+
+// global stream finish + router + mixer LayerNorm (model.py:128-153)
+template <int NV>
+__global__ void __launch_bounds__(32 * kRowWarps) k_mix_fwd_w(ModelPtrs M) {
+  ROW_PROLOGUE
+  // count this step's roll of the ring-buffer cache (see k_mix_fwd)
+  if (M.ring_on && b == 0 && lane == 0) M.st->ring += 1;
+  const VFlags vf = vflags(M.variant);
+  const float lam = M.w[P_LAM_MEM].p[0];
+  RowV<NV> hg, hm, up, x, hl, rp;
+  if (vf.global) {
+    up = ld_split<NV>(M.a.ws_mem, plane, rH, M.splits_mem);
+    x = ld_row<NV>(M.a.x + rH);
+  }
+  if (vf.local) hl = ld_row<NV>(M.a.h_l + rH);
+  if (vf.router) rp = ld_split<NV>(M.sk[S_RPRE].ws, plane, rH, M.sk[S_RPRE].S);
+  float asum = 0.f, amin = 3.4e38f, amax = -3.4e38f;
+  RowV<NV> al;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float g = 0.f, h;
+      if (vf.global) g = gelu_f(el(up.v[k], e)) + el(x.v[k], e) * lam;
+      if (vf.router) {
+        const float a = sigmoid_f(el(rp.v[k], e));
+        h = a * g + (1.0f - a) * el(hl.v[k], e);
+        el(al.v[k], e) = a;
+        asum += a;
+        amin = fminf(amin, a);
+        amax = fmaxf(amax, a);
+      } else {
+        h = vf.global ? g : el(hl.v[k], e);
+      }
+      el(hg.v[k], e) = g;
+      el(hm.v[k], e) = h;
+    }
+  if (vf.global) {
+    st_row<NV>(M.a.upre + rH, up);
+    st_row<NV>(M.a.h_g + rH, hg);
+  }
+  st_row<NV>(M.a.h_mix + rH, hm);
+  if (vf.router) {
+    st_row<NV>(M.a.alpha + rH, al);
+    const float s = warp_sum(asum);
+    const float mn = -warp_max(-amin), mx = warp_max(amax);
+    if (lane == 0) {
+      M.a.alpha_row[3 * b + 0] = s;
+      M.a.alpha_row[3 * b + 1] = mn;
+      M.a.alpha_row[3 * b + 2] = mx;
+    }
+  }
+  if (!vf.mixer) return;
+  float mu, inv;
+  row_ln_stats<NV>(hm, (float)H, &mu, &inv);
+  const RowV<NV> g = ld_row<NV>(M.w[P_MIX_LN_G].p), bb = ld_row<NV>(M.w[P_MIX_LN_B].p);
+  RowV<NV> zh, z;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float t = (el(hm.v[k], e) - mu) * inv;
+      el(zh.v[k], e) = t;
+      el(z.v[k], e) = t * el(g.v[k], e) + el(bb.v[k], e);
+    }
+  st_row<NV>(M.a.z_hat + rH, zh);
+  st_row<NV>(M.a.z + rH, z);
+  if (lane == 0) M.a.z_inv[b] = inv;
+}
+
+// self-gated coarse refiner + FNR LayerNorm (model.py:156-167)
+template <int NV>
+__global__ void __launch_bounds__(32 * kRowWarps) k_coarse_fwd_w(ModelPtrs M) {
+  ROW_PROLOGUE
+  const VFlags vf = vflags(M.variant);
+  const float lam = M.w[P_LAM_MIX].p[0];
+  const RowV<NV> in = ld_split<NV>(M.sk[S_INNER].ws, plane, rH, M.sk[S_INNER].S);
+  const RowV<NV> hm = ld_row<NV>(M.a.h_mix + rH);
+  RowV<NV> cp, gt, hc;
+  if (vf.gate) cp = ld_split<NV>(M.sk[S_CPRE].ws, plane, rH, M.sk[S_CPRE].S);
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float t = vf.gate ? sigmoid_f(el(cp.v[k], e)) : 1.0f;   // mixer_nogate: inner * 1
+      el(gt.v[k], e) = t;
+      el(hc.v[k], e) = el(in.v[k], e) * t + el(hm.v[k], e) * lam;
+    }
+  st_row<NV>(M.a.inner + rH, in);
+  st_row<NV>(M.a.gate + rH, gt);
+  st_row<NV>(M.a.h_c + rH, hc);
+  if (!vf.fnr) return;
+  float mu, inv;
+  row_ln_stats<NV>(hc, (float)H, &mu, &inv);
+  const RowV<NV> g = ld_row<NV>(M.w[P_REF_LN_G].p), bb = ld_row<NV>(M.w[P_REF_LN_B].p);
+  RowV<NV> zh, z;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float t = (el(hc.v[k], e) - mu) * inv;
+      el(zh.v[k], e) = t;
+      el(z.v[k], e) = t * el(g.v[k], e) + el(bb.v[k], e);
+    }
+  st_row<NV>(M.a.z2_hat + rH, zh);
+  st_row<NV>(M.a.z2 + rH, z);
+  if (lane == 0) M.a.z2_inv[b] = inv;
+}
+
+// FNR output: split-K reduce, LayerNorm, gelu, residual (model.py:170-172)
+template <int NV>
+__global__ void __launch_bounds__(32 * kRowWarps) k_out_fwd_w(ModelPtrs M) {
+  ROW_PROLOGUE
+  const RowV<NV> np = ld_split<NV>(M.a.ws_f, plane, rH, M.splits_f);
+  const RowV<NV> hc = ld_row<NV>(M.a.h_c + rH);
+  const RowV<NV> g = ld_row<NV>(M.w[P_OUT_LN_G].p), bb = ld_row<NV>(M.w[P_OUT_LN_B].p);
+  const float lam = M.w[P_LAM_OUT].p[0];
+  float mu, inv;
+  row_ln_stats<NV>(np, (float)H, &mu, &inv);
+  RowV<NV> nh, nv, h;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float t = (el(np.v[k], e) - mu) * inv;
+      const float v = t * el(g.v[k], e) + el(bb.v[k], e);
+      el(nh.v[k], e) = t;
+      el(nv.v[k], e) = v;
+      el(h.v[k], e) = gelu_f(v) + el(hc.v[k], e) * lam;
+    }
+  st_row<NV>(M.a.n_hat + rH, nh);
+  st_row<NV>(M.a.nrm + rH, nv);
+  st_row<NV>(M.a.h + rH, h);
+  if (lane == 0) M.a.n_inv[b] = inv;
+}
+
+// ---------------------------------------------------------------------------
+// backward
+
+// LayerNorm backward means (ops.py:103-113): m1 = mean(dy*g), m2 = mean(dy*g*xhat)
+template <int NV>
+__device__ __forceinline__ void row_ln_bwd_means(const RowV<NV>& dy, const RowV<NV>& g,
+                                                 const RowV<NV>& xh, float n, float* m1, float* m2) {
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float gg = el(dy.v[k], e) * el(g.v[k], e);
+      s1 += gg;
+      s2 += gg * el(xh.v[k], e);
+    }
+  *m1 = warp_sum(s1) / n;
+  *m2 = warp_sum(s2) / n;
+}
+
+// h = gelu(LN(npre)) + lam_out * h_c   (model.py:170-172 backward)
+template <int NV>
+__global__ void __launch_bounds__(32 * kRowWarps) k_out_bwd_w(ModelPtrs M) {
+  ROW_PROLOGUE
+  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  const float lam = M.w[P_LAM_OUT].p[0];
+  const RowV<NV> dh = ld_split<NV>(M.sk[S_DH].ws, plane, rH, M.sk[S_DH].S);
+  const RowV<NV> nrm = ld_row<NV>(M.a.nrm + rH), nh = ld_row<NV>(M.a.n_hat + rH);
+  const RowV<NV> hc = ld_row<NV>(M.a.h_c + rH), g = ld_row<NV>(M.w[P_OUT_LN_G].p);
+  const float inv = M.a.n_inv[b];
+  RowV<NV> dn, rg, dhc;
+  float lsum = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float d = el(dh.v[k], e);
+      const float v = d * gelu_grad_f(el(nrm.v[k], e));
+      el(dn.v[k], e) = v;
+      el(rg.v[k], e) = v * el(nh.v[k], e);
+      lsum += d * el(hc.v[k], e);
+      el(dhc.v[k], e) = d * lam;
+    }
+  st_row<NV>(rr + M.sl.out_g, rg);
+  st_row<NV>(rr + M.sl.out_b, dn);
+  st_row<NV>(M.a.dhc + rH, dhc);
+  const float ls = warp_sum(lsum);
+  if (lane == 0) rr[M.sl.lam_out] = ls;
+  float m1, m2;
+  row_ln_bwd_means<NV>(dn, g, nh, (float)H, &m1, &m2);
+  RowV<NV> dx;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      el(dx.v[k], e) = (el(dn.v[k], e) * el(g.v[k], e) - m1 - el(nh.v[k], e) * m2) * inv;
+  st_row<NV>(M.a.dnpre + rH, dx);
+}
+
+// z2 = LN(h_c); h_c = inner * sigmoid(cpre) + lam_mix * h_mix   (backward)
+template <int NV>
+__global__ void __launch_bounds__(32 * kRowWarps) k_coarse_bwd_w(ModelPtrs M) {
+  ROW_PROLOGUE
+  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  const VFlags vf = vflags(M.variant);
+  RowV<NV> dhc;
+  if (vf.fnr) {
+    const RowV<NV> dz = ld_split<NV>(M.a.ws_dz2, plane, rH, M.splits_dz2);
+    const RowV<NV> zh = ld_row<NV>(M.a.z2_hat + rH), g = ld_row<NV>(M.w[P_REF_LN_G].p);
+    const RowV<NV> din = ld_row<NV>(M.a.dhc + rH);
+    const float inv = M.a.z2_inv[b];
+    RowV<NV> rg;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) el(rg.v[k], e) = el(dz.v[k], e) * el(zh.v[k], e);
+    st_row<NV>(rr + M.sl.ref_g, rg);
+    st_row<NV>(rr + M.sl.ref_b, dz);
+    float m1, m2;
+    row_ln_bwd_means<NV>(dz, g, zh, (float)H, &m1, &m2);
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        el(dhc.v[k], e) = el(din.v[k], e) +
+                          (el(dz.v[k], e) * el(g.v[k], e) - m1 - el(zh.v[k], e) * m2) * inv;
+  } else {
+    // without the FNR, h = h_coarse and dh arrives straight from the head GEMM
+    dhc = ld_split<NV>(M.sk[S_DH].ws, plane, rH, M.sk[S_DH].S);
+  }
+  const RowV<NV> gt = ld_row<NV>(M.a.gate + rH), hm = ld_row<NV>(M.a.h_mix + rH);
+  RowV<NV> inner, di, dc;
+  if (vf.gate) inner = ld_row<NV>(M.a.inner + rH);
+  float lsum = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float d = el(dhc.v[k], e), t = el(gt.v[k], e);
+      el(di.v[k], e) = d * t;
+      if (vf.gate) el(dc.v[k], e) = d * el(inner.v[k], e) * t * (1.0f - t);
+      lsum += d * el(hm.v[k], e);
+    }
+  st_row<NV>(M.a.dhc + rH, dhc);
+  st_row<NV>(M.a.dinner + rH, di);
+  if (vf.gate) st_row<NV>(M.a.dcpre + rH, dc);
+  const float ls = warp_sum(lsum);
+  if (lane == 0) rr[M.sl.lam_mix] = ls;
+}
+
+// mixer LayerNorm + router mix + global-stream gelu (model.py:128-153 backward)
+template <int NV>
+__global__ void __launch_bounds__(32 * kRowWarps) k_mix_bwd_w(ModelPtrs M) {
+  ROW_PROLOGUE
+  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  const VFlags vf = vflags(M.variant);
+  RowV<NV> dhm;
+  if (vf.mixer) {
+    const RowV<NV> dz = ld_split<NV>(M.sk[S_DZ].ws, plane, rH, M.sk[S_DZ].S);
+    const RowV<NV> zh = ld_row<NV>(M.a.z_hat + rH), g = ld_row<NV>(M.w[P_MIX_LN_G].p);
+    const RowV<NV> dc = ld_row<NV>(M.a.dhc + rH);
+    RowV<NV> dm;
+    if (vf.gate) dm = ld_split<NV>(M.sk[S_DHMC].ws, plane, rH, M.sk[S_DHMC].S);
+    const float inv = M.a.z_inv[b];
+    const float lam_mix = M.w[P_LAM_MIX].p[0];
+    RowV<NV> rg;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) el(rg.v[k], e) = el(dz.v[k], e) * el(zh.v[k], e);
+    st_row<NV>(rr + M.sl.mix_g, rg);
+    st_row<NV>(rr + M.sl.mix_b, dz);
+    float m1, m2;
+    row_ln_bwd_means<NV>(dz, g, zh, (float)H, &m1, &m2);
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        el(dhm.v[k], e) = el(dc.v[k], e) * lam_mix + (vf.gate ? el(dm.v[k], e) : 0.f) +
+                          (el(dz.v[k], e) * el(g.v[k], e) - m1 - el(zh.v[k], e) * m2) * inv;
+  } else {
+    dhm = ld_split<NV>(M.sk[S_DH].ws, plane, rH, M.sk[S_DH].S);   // h = h_mix
+  }
+  const float lam_mem = M.w[P_LAM_MEM].p[0];
+  RowV<NV> al, hg, hl, up, x;
+  if (vf.router) {
+    al = ld_row<NV>(M.a.alpha + rH);
+    hg = ld_row<NV>(M.a.h_g + rH);
+    hl = ld_row<NV>(M.a.h_l + rH);
+  }
+  if (vf.global) {
+    up = ld_row<NV>(M.a.upre + rH);
+    x = ld_row<NV>(M.a.x + rH);
+  }
+  RowV<NV> drp, dl, dup, dxp;
+  float lsum = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float d = el(dhm.v[k], e);
+      float dg = d, dlc = d;
+      if (vf.router) {
+        const float a = el(al.v[k], e);
+        const float da = d * (el(hg.v[k], e) - el(hl.v[k], e));
+        dg = d * a;
+        dlc = d * (1.0f - a);
+        el(drp.v[k], e) = da * a * (1.0f - a);
+      }
+      el(dl.v[k], e) = dlc;
+      if (vf.global) {
+        el(dup.v[k], e) = dg * gelu_grad_f(el(up.v[k], e));
+        el(dxp.v[k], e) = dg * lam_mem;
+        lsum += dg * el(x.v[k], e);
+      }
+    }
+  if (vf.router) st_row<NV>(M.a.drpre + rH, drp);
+  if (vf.local) st_row<NV>(M.a.dh_l + rH, dl);
+  if (!vf.global) return;
+  st_row<NV>(M.a.dupre + rH, dup);
+  st_row<NV>(M.a.dx_part + rH, dxp);
+  const float ls = warp_sum(lsum);
+  if (lane == 0) rr[M.sl.lam_mem] = ls;
+}
+
+// ---------------------------------------------------------------------------
+// dispatch: returns false when the geometry needs the CTA-per-row kernels
+
+#define ROW_LAUNCH(kern)                                                              \
+  bool launch_##kern##_w(const ModelPtrs& M, cudaStream_t s) {                         \
+    if (M.d.H % 128 || M.d.H > 1024) return false;                                     \
+    const dim3 grid(cdiv(M.d.B, kRowWarps)), block(32 * kRowWarps);                    \
+    switch (M.d.H / 128) {                                                             \
+      case 1: launch_pdl(k_##kern##_w<1>, grid, block, 0, s, M); return true;          \
+      case 2: launch_pdl(k_##kern##_w<2>, grid, block, 0, s, M); return true;          \
+      case 4: launch_pdl(k_##kern##_w<4>, grid, block, 0, s, M); return true;          \
+      case 8: launch_pdl(k_##kern##_w<8>, grid, block, 0, s, M); return true;          \
+    }                                                                                  \
+    return false;                                                                      \
+  }
+
+ROW_LAUNCH(mix_fwd)
+ROW_LAUNCH(coarse_fwd)
+ROW_LAUNCH(out_fwd)
+ROW_LAUNCH(out_bwd)
+ROW_LAUNCH(coarse_bwd)
+ROW_LAUNCH(mix_bwd)
+
+}  // namespace fade

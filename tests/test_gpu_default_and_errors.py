@@ -272,3 +272,36 @@ def _ring_check():
     st["cache"] = np.arange(cfg.batch * cfg.cache_dim, dtype=np.float32).reshape(cfg.batch, -1)
     m.load_state(st)
     np.testing.assert_array_equal(m.save_state()["cache"], st["cache"])
+
+
+def test_warp_row_kernels_at_large_batch():
+    """B >= 2048 runs the warp-per-row row kernels (row_warp.cu): probabilities
+    and losses track the CPU oracle over a few online steps (H = 128 and 512
+    instantiations), and a compress -> decompress round trip is lossless with
+    the decoder replaying the encoder's losses bit for bit."""
+    from oracle.model import OracleModel
+    from paper_2604_07239_b200 import ModelConfig, corpus
+    from paper_2604_07239_b200.model import Predictor
+    from paper_2604_07239_b200.pipeline import run_parallel_decompress, run_pipelined_compress
+    for dims in (dict(ctx_len=8, embed_dim=16, cache_dim=256, mix_dim=32, expand_dim=256),
+                 dict(ctx_len=16, embed_dim=32, cache_dim=512, mix_dim=32, expand_dim=512)):
+        cfg = ModelConfig(batch=2048, workers=1, seed=9, **dims)
+        T = cfg.ctx_len
+        L = T + 4
+        mat = np.frombuffer(corpus.make_text(cfg.batch * L, 6), np.uint8).reshape(cfg.batch, L)
+        m, o = Predictor(cfg), OracleModel(cfg)
+        for i in range(T, T + 3):
+            p, q = m.predict(mat[:, i - T:i]), o.predict(mat[:, i - T:i])
+            assert np.abs(p - q).max() < 2e-3, (dims, i)
+            lg, lr = m.train_step(mat[:, i]), o.train_step(mat[:, i])
+            assert abs(lg - lr) < 2e-3 * max(1.0, abs(lr)), (dims, i)
+    cfg = ModelConfig(batch=2048, workers=1, seed=9, ctx_len=8, embed_dim=16, cache_dim=256,
+                      mix_dim=32, expand_dim=256)
+    data = corpus.make_text(2048 * 24, 8)
+    res = run_pipelined_compress(data, cfg)
+    lengths = np.array([len(s) for s in res.streams], np.int64)
+    offsets = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+    out, losses = run_parallel_decompress(np.frombuffer(b"".join(res.streams), np.uint8), offsets,
+                                          lengths, res.cfg, len(data), want_losses=True)
+    assert out == data
+    assert losses == res.losses

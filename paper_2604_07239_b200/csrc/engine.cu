@@ -351,7 +351,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   // ablation variants (model.py:121-175) drop whole GEMMs; an empty launch
   // group is a no-op
   const VFlags vf = vflags(M.variant);
-  float* h_final = vf.fnr ? a.h : (vf.mixer ? a.h_c : a.h_mix);
+  float* h_final = vf.fnr ? a.h : (vf.mixer ? a.h_c : a.hm_tc);
   // the cache operand of the W_mem GEMMs is a ring buffer (allocate: ring_on)
   // (the forward GEMM runs before mix_fwd counts this step's roll: bias 1)
   auto ring_operand = [&](GemmDesc& g, int kind) {
@@ -374,7 +374,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   {
     auto bl = b(G_ROUTE_MEM);
     if (vf.router)
-      TRY(bl.add(sk(gd(a.x, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_RPRE)));
+      TRY(bl.add(sk(gd(a.x_tc, H, 0, w[P_W_ROUTE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_RPRE)));
     GemmDesc g = gd(a.cache, C, 0, w[P_W_MEM].p, H, 0, B, H, C, EPI_STORE, a.ws_mem, H);
     g.splits = M.splits_mem;
     ring_operand(g, 1);
@@ -385,7 +385,7 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     auto bl = b(G_UP_CGATE);
     TRY(bl.add(sk(gd(a.u, X, 0, w[P_W_UP].p, H, 0, B, H, X, EPI_STORE, nullptr, 0), S_INNER)));
     if (vf.gate)
-      TRY(bl.add(sk(gd(a.h_mix, H, 0, w[P_W_CGATE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_CPRE)));
+      TRY(bl.add(sk(gd(a.hm_tc, H, 0, w[P_W_CGATE].p, H, 0, B, H, H, EPI_STORE, nullptr, 0), S_CPRE)));
   }
   if (vf.fnr) {
     GemmDesc g = gd(a.z2, H, 0, w[P_W_E1].p, 2LL * Ep, 0, B, 2 * Ep, H, EPI_GEGLU, a.a12, 2LL * Ep);
@@ -464,13 +464,13 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     auto bl = b(G_WUP_WCGATE);
     TRY(bl.add(adam(gd(a.u, X, 1, a.dinner, H, 0, X, H, B, EPI_ADAM, nullptr, H), w[P_W_UP])));
     if (vf.gate)
-      TRY(bl.add(adam(gd(a.h_mix, H, 1, a.dcpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_CGATE])));
+      TRY(bl.add(adam(gd(a.hm_tc, H, 1, a.dcpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_CGATE])));
     TRY(bl.add(adam(gd(a.z, H, 1, a.dzd, X, 0, H, X, B, EPI_ADAM, nullptr, X), w[P_W_DOWN])));
   }
   {
     auto bl = b(G_WROUTE_WMEM);
     if (vf.router)
-      TRY(bl.add(adam(gd(a.x, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE])));
+      TRY(bl.add(adam(gd(a.x_tc, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE])));
     if (vf.global) {
       GemmDesc g = gd(a.cache, C, 1, a.dupre, H, 0, C, H, B, EPI_ADAM, nullptr, H);
       ring_operand(g, 2);
@@ -557,7 +557,7 @@ static int allocate(fade_model* m) {
   float *sp, *smm, *sv, *sg;
   F(&sp, m->sl.total); F(&smm, m->sl.total); F(&sv, m->sl.total); F(&sg, m->sl.total);
   Acts& a = M.a;
-  F(&a.x, B * H); F(&a.x_hat, B * H); F(&a.x_inv, B); F(&a.gpre, B * d.D); F(&a.vpre, B * d.D);
+  F(&a.x, B * H); F(&a.x_tc, B * H); F(&a.hm_tc, B * H); F(&a.x_hat, B * H); F(&a.x_inv, B); F(&a.gpre, B * d.D); F(&a.vpre, B * d.D);
   F(&a.loc, B * H); F(&a.loc_hat, B * H); F(&a.loc_inv, B * d.T); F(&a.conv_pre, B * H);
   F(&a.h_l, B * H); F(&a.cache, B * C);
   F(&a.ws_mem, (long long)M.splits_mem * B * H); F(&a.upre, B * H); F(&a.h_g, B * H);

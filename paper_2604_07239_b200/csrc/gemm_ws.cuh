@@ -291,9 +291,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
             for (int k = 0; k < 16; k += 4) {
               *etile_at(eb, r, c + k) = make_float4(a1[k], a1[k + 1], a1[k + 2], a1[k + 3]);
               *etile_at(eb + kWsSub, r, c + k) = make_float4(a2[k], a2[k + 1], a2[k + 2], a2[k + 3]);
+              // wide is only a GEMM operand (F, W_f update): stored TF32-rounded
               *etile_at(eb + 2 * kWsSub, r, c + k) =
-                  make_float4(gelu_f(a1[k]) * a2[k], gelu_f(a1[k + 1]) * a2[k + 1],
-                              gelu_f(a1[k + 2]) * a2[k + 2], gelu_f(a1[k + 3]) * a2[k + 3]);
+                  tf32_rne4(make_float4(gelu_f(a1[k]) * a2[k], gelu_f(a1[k + 1]) * a2[k + 1],
+                                        gelu_f(a1[k + 2]) * a2[k + 2], gelu_f(a1[k + 3]) * a2[k + 3]));
             }
           }
         } else {

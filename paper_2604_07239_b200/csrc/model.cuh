@@ -88,6 +88,9 @@ struct Acts {        // saved activations and gradient scratch, all [B][ld]
                                 //  in place each predict)
   float *ws_mem, *upre, *h_g, *alpha, *h_mix, *z_hat, *z_inv, *z;   // router pre-activation: sk[S_RPRE]
   float *zd, *u, *inner, *gate, *h_c, *z2_hat, *z2_inv, *z2;
+  // TF32-rounded copies of x and h_mix for their GEMMs (route / W_route
+  // update, cgate / W_cgate update): the fp32 originals also feed residuals
+  float *x_tc, *hm_tc;
   float *a12, *wide, *ws_f, *n_hat, *n_inv, *nrm, *h, *logits;
   double *probs;                // [B][256] (predict API only)
   unsigned *cum;                // [2][B][kCumLd] CSPP slots

@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     xs[j] = xv;
     M.a.x_hat[rH + j] = xh;
     M.a.x[rH + j] = xv;
+    M.a.x_tc[rH + j] = tf32_rne(xv);
   }
   if (tid == 0) M.a.x_inv[b] = inv;
   if constexpr (DT > 0) asm volatile("cp.async.wait_all;" ::: "memory");   // weights (and roll reads) landed
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
         }
         M.a.gpre[(long long)b * DT + tid] = gs;
         M.a.vpre[(long long)b * DT + tid] = vs;
-        *(ring ? ring_elem(tid) : crow + d.C - DT + tid) = gelu_f(gs) * vs;
+        *(ring ? ring_elem(tid) : crow + d.C - DT + tid) = tf32_rne(gelu_f(gs) * vs);
       }
       if (!ring)
         for (int q = tid; q < n4; q += blockDim.x) *(float4*)(crow + 4 * q) = *(const float4*)(cstage + 4 * q);
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     }
     M.a.gpre[(long long)b * d.D + o] = g;
     M.a.vpre[(long long)b * d.D + o] = v;
-    blk[o] = gelu_f(g) * v;
+    blk[o] = tf32_rne(gelu_f(g) * v);
   }
   // roll the cache in place: new[j] = old[j + D]; new[C-D+o] = block[o]
   if (ring) {
@@ -460,6 +461,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
       hmx = vf.global ? hg : M.a.h_l[rH + j];   // single-stream variants
     }
     M.a.h_mix[rH + j] = hmx;
+    M.a.hm_tc[rH + j] = tf32_rne(hmx);
     hm[j] = hmx;
   }
   __syncthreads();
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
   for (int j = tid; j < d.H; j += blockDim.x) {
     const float zh = (hm[j] - mu) * inv;
     M.a.z_hat[rH + j] = zh;
-    M.a.z[rH + j] = zh * g[j] + bb[j];
+    M.a.z[rH + j] = tf32_rne(zh * g[j] + bb[j]);
   }
   if (tid == 0) M.a.z_inv[b] = inv;
 }
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(32 * kBmmFwdWarps, 4) k_bmm_fwd(ModelPtrs M) {
     float u = 0.f;
 #pragma unroll
     for (int k = 0; k < kBmmFwdWarps; ++k) u += part[k * X + o];
-    M.a.u[(long long)b * X + o] = u;
+    M.a.u[(long long)b * X + o] = tf32_rne(u);
   }
 }
 
@@ -578,7 +580,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_fwd(ModelPtrs M) {
   for (int j = tid; j < d.H; j += blockDim.x) {
     const float zh = (hc[j] - mu) * inv;
     M.a.z2_hat[rH + j] = zh;
-    M.a.z2[rH + j] = zh * g[j] + bb[j];
+    M.a.z2[rH + j] = tf32_rne(zh * g[j] + bb[j]);
   }
   if (tid == 0) M.a.z2_inv[b] = inv;
 }
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_out_fwd(ModelPtrs M) {
     const float nv = nh * g[j] + bb[j];
     M.a.n_hat[rH + j] = nh;
     M.a.nrm[rH + j] = nv;
-    M.a.h[rH + j] = gelu_f(nv) + M.a.h_c[rH + j] * lam;
+    M.a.h[rH + j] = tf32_rne(gelu_f(nv) + M.a.h_c[rH + j] * lam);
   }
   if (tid == 0) M.a.n_inv[b] = inv;
 }

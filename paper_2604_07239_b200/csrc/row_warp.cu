@@ -46,6 +46,13 @@ __device__ __forceinline__ float& el(float4& f, int e) {
 __device__ __forceinline__ float el(const float4& f, int e) {
   return e == 0 ? f.x : (e == 1 ? f.y : (e == 2 ? f.z : f.w));
 }
+// GEMM-only operands stored rounded to nearest TF32 (common.cuh tf32_rne)
+template <int NV>
+__device__ __forceinline__ RowV<NV> rne_row(RowV<NV> r) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) r.v[k] = tf32_rne4(r.v[k]);
+  return r;
+}
 template <int NV>
 __device__ __forceinline__ float row_sum(const RowV<NV>& r) {
   float s = 0.f;
@@ -152,6 +159,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_mix_fwd_w(ModelPtrs M) {
     st_row<NV>(M.a.h_g + rH, hg);
   }
   st_row<NV>(M.a.h_mix + rH, hm);
+  st_row<NV>(M.a.hm_tc + rH, rne_row<NV>(hm));
   if (vf.router) {
     st_row<NV>(M.a.alpha + rH, al);
     const float s = warp_sum(asum);
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_mix_fwd_w(ModelPtrs M) {
       el(z.v[k], e) = t * el(g.v[k], e) + el(bb.v[k], e);
     }
   st_row<NV>(M.a.z_hat + rH, zh);
-  st_row<NV>(M.a.z + rH, z);
+  st_row<NV>(M.a.z + rH, rne_row<NV>(z));
   if (lane == 0) M.a.z_inv[b] = inv;
 }
 
@@ -215,7 +223,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_coarse_fwd_w(ModelPtrs M) {
       el(z.v[k], e) = t * el(g.v[k], e) + el(bb.v[k], e);
     }
   st_row<NV>(M.a.z2_hat + rH, zh);
-  st_row<NV>(M.a.z2 + rH, z);
+  st_row<NV>(M.a.z2 + rH, rne_row<NV>(z));
   if (lane == 0) M.a.z2_inv[b] = inv;
 }
 
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_out_fwd_w(ModelPtrs M) {
     }
   st_row<NV>(M.a.n_hat + rH, nh);
   st_row<NV>(M.a.nrm + rH, nv);
-  st_row<NV>(M.a.h + rH, h);
+  st_row<NV>(M.a.h + rH, rne_row<NV>(h));
   if (lane == 0) M.a.n_inv[b] = inv;
 }
 

@@ -52,7 +52,7 @@ def test_default_geometry_matches_reference_digest():
         ref = z["probs"][j]
         got = p[:ref.shape[0]]
         assert np.abs(got - ref).max() < 1e-3, (j, float(np.abs(got - ref).max()))
-        assert kl_bits(ref, got) < 1e-5, (j, kl_bits(ref, got))
+        assert kl_bits(ref, got) < 1e-6, (j, kl_bits(ref, got))
         loss = m.train_step(mat[:, i])
         assert abs(loss - float(z["losses"][j])) < 1e-3 * float(z["losses"][j]), (j, loss)
     # the first 4096 elements of every parameter after the three updates

@@ -1,12 +1,15 @@
 """Predictor on the B200 vs the reference, from transplanted reference state.
 
 Tolerances (north_star "stated tolerance"): the GEMMs run
-on TF32 tensor cores, which TRUNCATE the operand mantissas to 10 bits.  A numpy
-emulation of that truncation on the same golden state gives max-abs 7e-4 and
-mean KL 4.2e-6 bits/symbol (round-to-nearest would give 2.3e-8;
-tests/test_oracle.py::test_tf32_truncation_budget), so one-step probabilities
-must match the reference within max-abs 1e-3 and mean KL 1e-5 bits/symbol --
-about 6e-6 of a bit per byte, far inside the 0.5% bits/byte gate; intermediates within 2e-3
+on TF32 tensor cores, which TRUNCATE the operand mantissas to 10 bits.  The
+activations that are only ever GEMM operands are stored already rounded to
+nearest TF32 (x and h_mix through rounded copies), which leaves only the
+weight operand truncated: tools/precision_study.py emulates that at KL
+9.3e-7 / 3.9e-7 bits/symbol on the tiny / mid golden states (3.8e-6 / 1.5e-6
+with both operands truncated), and the device measures 9.2e-7 / 4.1e-7.  So
+one-step probabilities must match the reference within max-abs 1e-3 and mean
+KL 1e-6 bits/symbol (SURVEY.md's proposed gate) -- about 1e-6 of a bit per
+byte, far inside the 0.5% bits/byte gate; intermediates within 2e-3
 relative to their scale; gradients within 2e-2 relative (TF32 through the
 whole backward); one Adam step within 2.5*lr per element (Adam normalises,
 so near-zero gradients may change sign) with a median far below lr.
@@ -63,7 +66,7 @@ def test_predict_probabilities(name):
     p = m.predict(z["ctx"])
     ref = z["next_probs"]
     assert np.abs(p - ref).max() < 1e-3
-    assert kl_bits(ref, p) < 1e-5
+    assert kl_bits(ref, p) < 1e-6
     np.testing.assert_allclose(p.sum(axis=1), 1.0, atol=1e-12)
     assert (p > 0).all()
     assert 0.0 < m.alpha_stats[1] <= m.alpha_stats[0] <= m.alpha_stats[2] < 1.0

@@ -145,7 +145,7 @@ bool launch_out_fwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_out_bwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_coarse_bwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_mix_bwd_w(const ModelPtrs& M, cudaStream_t s);
-bool row_warp_enabled(int B);
+bool row_warp_enabled(int B, int which);   // which: 0 mix_fwd .. 5 mix_bwd
 
 // row kernels (model_kernels.cu)
 void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,

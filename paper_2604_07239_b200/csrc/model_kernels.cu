@@ -14,9 +14,9 @@ namespace fade {
 // Measured per B (timestep, same box): B = 512 336 -> 364 us, 1024 530 ->
 // 547 us (one warp per row is too little parallelism per row when the grid is
 // small), 2048 883 -> 844 us, 4096 1631 -> 1547 us; so B >= 2048 only.
-bool row_warp_enabled(int B) {
+bool row_warp_enabled(int B, int which) {
   static const int forced = knob("FADE_ROW_WARP") ? atoi(knob("FADE_ROW_WARP")) : -1;
-  if (forced >= 0) return forced != 0;
+  if (forced >= 0) return (forced >> which) & 1;   // experiments: a bit per kernel
   return B >= 2048;
 }
 
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
 }
 
 void launch_mix_fwd(const ModelPtrs& M, cudaStream_t s) {
-  if (row_warp_enabled(M.d.B) && launch_mix_fwd_w(M, s)) return;
+  if (row_warp_enabled(M.d.B, 0) && launch_mix_fwd_w(M, s)) return;
   launch_pdl(k_mix_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (6 * M.d.H + 32), s,
              M);
 }
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_fwd(ModelPtrs M) {
 }
 
 void launch_coarse_fwd(const ModelPtrs& M, cudaStream_t s) {
-  if (row_warp_enabled(M.d.B) && launch_coarse_fwd_w(M, s)) return;
+  if (row_warp_enabled(M.d.B, 1) && launch_coarse_fwd_w(M, s)) return;
   launch_pdl(k_coarse_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_out_fwd(ModelPtrs M) {
 }
 
 void launch_out_fwd(const ModelPtrs& M, cudaStream_t s) {
-  if (row_warp_enabled(M.d.B) && launch_out_fwd_w(M, s)) return;
+  if (row_warp_enabled(M.d.B, 2) && launch_out_fwd_w(M, s)) return;
   launch_pdl(k_out_fwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (5 * M.d.H + 32), s,
              M);
 }
@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_out_bwd(ModelPtrs M) {
 }
 
 void launch_out_bwd(const ModelPtrs& M, cudaStream_t s) {
-  if (row_warp_enabled(M.d.B) && launch_out_bwd_w(M, s)) return;
+  if (row_warp_enabled(M.d.B, 3) && launch_out_bwd_w(M, s)) return;
   launch_pdl(k_out_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 
@@ -927,7 +927,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_coarse_bwd(ModelPtrs M) {
 }
 
 void launch_coarse_bwd(const ModelPtrs& M, cudaStream_t s) {
-  if (row_warp_enabled(M.d.B) && launch_coarse_bwd_w(M, s)) return;
+  if (row_warp_enabled(M.d.B, 4) && launch_coarse_bwd_w(M, s)) return;
   launch_pdl(k_coarse_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (5 * M.d.H + 32),
              s, M);
 }
@@ -1200,7 +1200,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_bwd(ModelPtrs M) {
 }
 
 void launch_mix_bwd(const ModelPtrs& M, cudaStream_t s) {
-  if (row_warp_enabled(M.d.B) && launch_mix_bwd_w(M, s)) return;
+  if (row_warp_enabled(M.d.B, 5) && launch_mix_bwd_w(M, s)) return;
   launch_pdl(k_mix_bwd, dim3(M.d.B), dim3(row_threads(M.d.H)), sizeof(float) * (M.d.H + 32), s, M);
 }
 

@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=30, help="CPU-port timesteps (~10 s of host work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--sweep-batches", default="64,128,256,512,1024,2048,4096")
+    ap.add_argument("--sweep-bytes", type=int, default=2 << 20,
+                    help="per-B compress_bytes sample for bits/byte")
     return ap.parse_args()
 
 
@@ -204,6 +208,53 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def batch_sweep(args, lib, data, hbm, tf32):
+    """BASELINE.json config 3 on this GPU: for each B, the device-resident
+    timestep (graph replays, CUDA events on the model stream, after warm-up)
+    against its roofline, and the bits/byte of a
+    compress_bytes call on a fixed sample at that B (lossless checked)."""
+    import torch
+    from paper_2604_07239_b200 import ModelConfig, _native, container
+    from paper_2604_07239_b200.model import Predictor
+    from paper_2604_07239_b200.pipeline import StreamPartition
+    rows = []
+    sample = data[:args.sweep_bytes]
+    for b in [int(x) for x in args.sweep_batches.split(",")]:
+        cfg = ModelConfig(batch=b, workers=1)
+        part = StreamPartition.from_length(min(len(data), b * 2048), b)
+        mat = torch.from_numpy(np.ascontiguousarray(part.split(data[:part.original_length]))).cuda()
+        m = Predictor(cfg)
+        sp = ctypes.c_void_p()
+        lib.fade_model_stream(m.handle, ctypes.byref(sp))
+        stream = torch.cuda.ExternalStream(sp.value)
+        coder, la = ctypes.c_void_p(), ctypes.c_int()
+        run = lambda n: _native.check(lib.fade_bench_compress_steps(
+            m.handle, mat.data_ptr(), part.stream_length, cfg.ctx_len, n, ctypes.byref(coder),
+            ctypes.byref(la), None), "steps")
+        run(8)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run(48)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 48
+        lib.fade_coder_destroy(coder)
+        del m, mat
+        blob, _ = container.compress_bytes(sample, cfg)
+        assert container.decompress_bytes(blob) == sample, f"round trip failed at B={b}"
+        P = 15_484_259 + 16_384 * b
+        t_roof = max(24.0 * P / (hbm * 1e9), 2.0 * b * 44_521_472 / (tf32 * 1e12))
+        rows.append({"batch": b, "us_per_timestep": round(ms * 1e3, 1),
+                     "MBps": round(b / ms / 1e3, 4), "roofline_MBps": round(b / t_roof / 1e6, 3),
+                     "roofline_frac": round(t_roof * 1e3 / ms, 4),
+                     "bound": "hbm" if 24.0 * P / hbm / 1e9 > 2.0 * b * 44_521_472 / tf32 / 1e12
+                     else "tensor",
+                     "bits_per_byte": round(8.0 * len(blob) / len(sample), 4)})
+        torch.cuda.empty_cache()
+    return {"sample_bytes": len(sample), "timesteps_timed": 48, "rows": rows}
 
 
 def run_ours(args):
@@ -381,6 +432,9 @@ def run_ours(args):
                "decompress_value": n / td / 1e6}
         dec = e2e["decompress_value"]
 
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        sweep = batch_sweep(args, lib, data, hbm, tf32)
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         base = cpu_baseline(cfg.batch, args.cpu_steps)
@@ -395,6 +449,7 @@ def run_ours(args):
                        "l2": "working set ~290 MB (params + Adam state) > 126 MB L2; no flush"},
             "decompress": dec, "gpu_launches": launches.value * K * S,
             "roofline": roof, "cpu_baseline": base, "e2e": e2e, "clocks": clk.summary(),
+            "batch_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if pg:

@@ -99,6 +99,7 @@ struct fade_model {
   cudaStream_t s_main = nullptr, s_side = nullptr, s_coder = nullptr;
   cudaEvent_t ev[8] = {};
   cudaEvent_t ev_cum[2] = {}, ev_enc[2] = {}, ev_side_done = nullptr, ev_coder_join = nullptr;
+  cudaEvent_t ev_wu[2] = {};    // W_U update forked off the model stream (experiments)
   void* mem = nullptr;
   ModelPtrs M;
   StepState* st = nullptr;      // device
@@ -452,14 +453,18 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   };
   // W_head rides in the W_f launch and W_down in the W_up/W_cgate launch:
   // fewer side-stream kernels (each costs a fixed ~10 us of latency)
+  // (experiments: FADE_MERGE_WF=1 puts W_head + W_f into the W12 launch, so
+  // their tiles follow W12's on the SMs it frees instead of queueing behind
+  // the model stream's kernels)
+  static const bool merge_wf = knob("FADE_MERGE_WF") && atoi(knob("FADE_MERGE_WF")) != 0;
+  if (vf.fnr)
+    TRY(b(G_W12).add(adam(gd(a.z2, H, 1, a.da12, 2LL * Ep, 0, H, 2 * Ep, B, EPI_ADAM, nullptr, 2LL * Ep), w[P_W_E1])));
   {
-    auto bl = b(G_WF);
+    auto bl = b(merge_wf && vf.fnr ? G_W12 : G_WF);
     TRY(bl.add(adam(gd(h_final, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD])));
     if (vf.fnr)
       TRY(bl.add(adam(gd(a.wide, Ep, 1, a.dnpre, H, 0, E, H, B, EPI_ADAM, nullptr, H), w[P_W_F])));
   }
-  if (vf.fnr)
-    TRY(b(G_W12).add(adam(gd(a.z2, H, 1, a.da12, 2LL * Ep, 0, H, 2 * Ep, B, EPI_ADAM, nullptr, 2LL * Ep), w[P_W_E1])));
   if (vf.mixer) {
     auto bl = b(G_WUP_WCGATE);
     TRY(bl.add(adam(gd(a.u, X, 1, a.dinner, H, 0, X, H, B, EPI_ADAM, nullptr, H), w[P_W_UP])));
@@ -739,9 +744,24 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   TRY(sides());
   // fused dzd + W_U Adam (mode 3): measured faster than moving the 201 MB W_U
   // RMW to the side stream (it then contends with the critical path for HBM)
+  // (experiments: FADE_WU_STREAM=1 / 2 keeps only the input gradient dzd on
+  // the model stream and runs the W_U read-modify-write on the coder / side
+  // stream, joined at the end of the step)
+  static const int wu_stream = knob("FADE_WU_STREAM") ? atoi(knob("FADE_WU_STREAM")) : 0;
+  bool wu_forked = false;
   if (vf.mixer) {
     L2Pin pin(m);
-    launch_bmm_bwd(M, grad_only, 3, s);
+    if (wu_stream) {
+      launch_bmm_bwd(M, grad_only, 1, s);
+      cudaStream_t ws = wu_stream == 1 ? m->s_coder : side;
+      CK(cudaEventRecord(m->ev_wu[0], s));
+      CK(cudaStreamWaitEvent(ws, m->ev_wu[0], 0));
+      launch_bmm_bwd(M, grad_only, 2, ws);
+      CK(cudaEventRecord(m->ev_wu[1], ws));
+      wu_forked = true;
+    } else {
+      launch_bmm_bwd(M, grad_only, 3, s);
+    }
   }
   TRY(sides());
   TRY(run_gemm(m, G_DZ, s));
@@ -755,6 +775,7 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   launch_small_adam(M, grad_only, losses, io.alpha_tape, advance, s);
   CK(cudaEventRecord(m->ev_side_done, side));
   CK(cudaStreamWaitEvent(s, m->ev_side_done, 0));
+  if (wu_forked) CK(cudaStreamWaitEvent(s, m->ev_wu[1], 0));
   CK(cudaGetLastError());
   return FADE_OK;
 }
@@ -930,6 +951,7 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   }
   CK(cudaEventCreateWithFlags(&m->ev_side_done, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&m->ev_coder_join, cudaEventDisableTiming));
+  for (auto& e : m->ev_wu) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   TRY(allocate(m.get()));
   if (l2_pin_mode(d)) {
     const size_t want = sizeof(float) * (size_t)d.B * d.X * d.X * (l2_pin_mode(d) == 2 ? 2 : 1);
@@ -966,6 +988,7 @@ int fade_model_destroy(fade_model_t* m) {
   }
   cudaEventDestroy(m->ev_side_done);
   cudaEventDestroy(m->ev_coder_join);
+  for (auto& e : m->ev_wu) cudaEventDestroy(e);
   cudaStreamDestroy(m->s_main);
   cudaStreamDestroy(m->s_side);
   cudaStreamDestroy(m->s_coder);

@@ -189,3 +189,19 @@ def test_bpb_fixture_has_reference_sizes():
     sizes = golden_json("bpb.json")
     assert sizes["default_text1m"]["bytes"] == 233320
     assert all(v["bytes"] > 0 for v in sizes.values())
+
+
+def test_torch_oracle_tracks_reference_trajectory():
+    """oracle/torch_model.py (the large-size bits/byte oracle, fp32 autograd +
+    the reference's Adam) reproduces the reference's 40-step trajectory from
+    the seeded init, on CPU here (the GPU runs it with TF32 disabled)."""
+    from oracle.torch_model import TorchOracle
+    cfg, _, z = model_golden("tiny")
+    m = TorchOracle(cfg, device="cpu")
+    mat, t = z["mat"], cfg.ctx_len
+    for j in range(z["probs"].shape[0]):
+        i = t + j
+        p = m.predict(mat[:, i - t:i]).numpy()
+        assert np.abs(p - z["probs"][j]).max() < 1e-4, j
+        loss = m.train_step(mat[:, i])
+        assert abs(loss - z["losses"][j]) < 1e-4, j

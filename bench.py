@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--chunk", type=int, default=64, help="timesteps per bench step")
     ap.add_argument("--batch", type=int, default=512)
     ap.add_argument("--size", type=int, default=100_000_000)
-    ap.add_argument("--e2e-bytes", type=int, default=8 << 20)
+    ap.add_argument("--e2e-bytes", type=int, default=32 << 20)
     ap.add_argument("--cpu-steps", type=int, default=30, help="CPU-port timesteps (~10 s of host work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

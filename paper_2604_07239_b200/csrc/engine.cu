@@ -157,6 +157,8 @@ static SmallLayout make_small_layout(const Dims& d) {
   s.loc_g = o; o += d.D;  s.loc_b = o; o += d.D;  s.conv_b = o; o += d.D;
   s.conv_k = o; o += d.K * d.D * d.D;
   s.w_gate = o; o += d.D * d.D;  s.w_val = o; o += d.D * d.D;
+  s.trunk0 = s.in_g;
+  s.trunk1 = o;   // in_g, in_b, loc_g, loc_b, conv_b, conv_k, w_gate, w_val
   s.lam_out = o++; s.lam_mix = o++; s.lam_mem = o++;
   // rowred rows start 16-byte aligned (the warp-per-row kernels store float4s);
   // the 0-3 padding slots stay zero: zero gradient, Adam leaves them at 0
@@ -330,9 +332,12 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   static const long pair_ids = knob("FADE_PAIR") ? atol(knob("FADE_PAIR"))
                                                    : (1L << G_W12) | (1L << G_DWIDE) |
                                                      (1L << G_DZ2) | (1L << G_F);
+  // (experiments: FADE_OCC2P = bit per GemmId, pair GEMMs at two CTAs per SM)
+  static const long occ2p_ids = knob("FADE_OCC2P") ? atol(knob("FADE_OCC2P")) : 0;
   for (int id = 0; id < G_COUNT; ++id) {
     if (!((pair_ids >> id) & 1) || m->bn[id] < 128) continue;
     Gs[id].pair = 2;
+    if ((occ2p_ids >> id) & 1) Gs[id].occ = 2;
     if (Gs[id].occ == 2) m->bn[id] = 256;   // pair tiles 256 x 256 at two CTAs per SM
   }
   // persistent warp-specialised kernel (gemm_ws.cuh) for the store/GeGLU GEMMs
@@ -580,6 +585,13 @@ static int allocate(fade_model* m) {
   F(&a.dcpre, B * H); F(&a.dzd, B * X);
   F(&a.drpre, B * H); F(&a.dupre, B * H); F(&a.dh_l, B * H); F(&a.dx_part, B * H);
   F(&a.rowred, B * m->sl.rowred);
+  {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    M.trunk_grid = (int)std::min<long long>(B, 4LL * sms);
+  }
+  F(&a.trunk_part, (long long)M.trunk_grid * (m->sl.trunk1 - m->sl.trunk0));
   const long long sk_width[S_COUNT] = {X, H, H, 256, H, X, H, H, H, d.D, H};
   for (int k = 0; k < S_COUNT; ++k) F(&M.sk[k].ws, (long long)M.sk[k].S * B * sk_width[k]);
   items.push_back({(void**)&a.emb_acc, sizeof(long long) * 256 * (size_t)d.D});

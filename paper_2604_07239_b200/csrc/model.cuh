@@ -57,6 +57,7 @@ struct SmallLayout {
   int w_gate, w_val;                                         // D*D each
   int lam_out, lam_mix, lam_mem;                             // 1 each
   int rowred;                                                // width of the rowred buffer
+  int trunk0, trunk1;   // [in_g, lam_out): the columns trunk_bwd sums per CTA (trunk_part)
   int b_head;                                                // 256, reduced from dlogits
   int total;
 };
@@ -100,6 +101,7 @@ struct Acts {        // saved activations and gradient scratch, all [B][ld]
   float *dlogits, *dhc, *dnpre, *da12, *ws_dz2, *dinner, *dcpre;
   float *dzd, *drpre, *dupre, *dh_l, *dx_part;
   float *rowred;                // [B][rowred]
+  float *trunk_part;            // [trunk_grid][trunk1 - trunk0] per-CTA sums of trunk_bwd
   long long* emb_acc;           // [256][D] embedding gradient, fixed point (emb_to_fixed)
 };
 
@@ -133,6 +135,9 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   // Layout then block-major, cache[(kb * B + b) * 32 + e] for physical
   // 32-column block kb, so the W_mem GEMMs read whole contiguous tiles.
   int ring_on;
+  // trunk_bwd grid: min(B, 4 per SM); each CTA loops over rows b = cta,
+  // cta + grid, ... and writes one partial row of its small-parameter sums
+  int trunk_grid;
 };
 __device__ __forceinline__ unsigned long long* tape_at(const ModelPtrs& M, int slot) {
   return M.tape + kTapeSlots * (M.st->col - M.st->loss_base) + slot;

@@ -1211,7 +1211,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   pdl_enter();
   Dims d = M.d;
   if (DT) { d.D = DT; d.T = TT; d.K = KT; d.H = DT * TT; }
-  const int b = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   extern __shared__ float sm[];
   float* dxs = sm;                        // [H] dx, later dxf
   float* dcv = dxs + d.H;                 // [H] dconv
@@ -1223,20 +1223,32 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   float* xt = dv + d.D;                   // [D]
   float* red = xt + d.D;                  // [32]
   int* ctx = (int*)(red + 32);            // [T] context symbols
-  const long long rH = (long long)b * d.H;
-  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+  // per-CTA sums of this kernel's small-parameter gradient columns
+  // [trunk0, trunk1) of the small arena (in_g ... w_val), accumulated over the
+  // CTA's rows in row order and written once to trunk_part[blockIdx.x]; the
+  // small-parameter kernel sums the gridDim.x partial rows in a fixed order
+  float* acc = (float*)(ctx + ((d.T + 3) & ~3));
+  const int t0 = M.sl.trunk0;
+  // rr[X + q] (a per-row column write of the CTA-per-row layout) becomes an
+  // accumulate into this CTA's partial row; each column has one owner thread
+#define RR_ADD(off, q, v) (acc[(off) - t0 + (q)] += (v))
   const float* Wg = M.w[P_W_GATE].p;
   const long long c0 = use_col ? M.st->col - d.T : 0;
-  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
   const float* Wv = M.w[P_W_VAL].p;
   // taps transposed to [tap][co][ci] with a padded row (D + 1) so both this
   // transposing store and the input-gradient loop below are bank-conflict free
+  // (once per CTA: the rows below share them)
   const int ckp = d.D + 1;
   for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) {
     const int tap = j / (d.D * d.D), ci = (j / d.D) % d.D, co = j % d.D;
     ck[(tap * d.D + co) * ckp + ci] = M.w[P_CONV_K].p[j];
   }
+  for (int c = tid; c < M.sl.trunk1 - t0; c += blockDim.x) acc[c] = 0.f;
   const VFlags vf = vflags(M.variant);
+  for (int b = blockIdx.x; b < d.B; b += gridDim.x) {
+  const long long rH = (long long)b * d.H;
+  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
+  __syncthreads();
   if (vf.global) {
     for (int o = tid; o < d.D; o += blockDim.x) {
       const float gp = M.a.gpre[(long long)b * d.D + o];
@@ -1263,8 +1275,8 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     // W_gate / W_val gradients (outer products) and dx_t
     for (int q = tid; q < d.D * d.D; q += blockDim.x) {
       const int i = q / d.D, o = q % d.D;
-      rr[M.sl.w_gate + q] = xt[i] * dg[o];
-      rr[M.sl.w_val + q] = xt[i] * dv[o];
+      RR_ADD(M.sl.w_gate, q, xt[i] * dg[o]);
+      RR_ADD(M.sl.w_val, q, xt[i] * dv[o]);
     }
     if constexpr (DT > 0) {
       // all 8 warps: warp w takes inputs i in [4w, 4w + 4), lane = output o
@@ -1293,8 +1305,8 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   // input LayerNorm backward
   const float* gin = M.w[P_IN_LN_G].p;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    rr[M.sl.in_g + j] = dxs[j] * M.a.x_hat[rH + j];
-    rr[M.sl.in_b + j] = dxs[j];
+    RR_ADD(M.sl.in_g, j, dxs[j] * M.a.x_hat[rH + j]);
+    RR_ADD(M.sl.in_b, j, dxs[j]);
   }
   float m1, m2;
   ln_bwd_means(dxs, M.a.x_hat + rH, gin, d.H, red, &m1, &m2);
@@ -1307,7 +1319,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   for (int co = tid; co < d.D; co += blockDim.x) {
     float s = 0.f;
     for (int t = 0; t < d.T; ++t) s += dcv[t * d.D + co];
-    rr[M.sl.conv_b + co] = s;
+    RR_ADD(M.sl.conv_b, co, s);
   }
   if constexpr (DT > 0) {
     // register-blocked: one (ci, co) pair per pass, its T inputs and T output
@@ -1322,13 +1334,13 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
       }
 #pragma unroll
       for (int tap = 0; tap < KT; ++tap) {
-        float acc = 0.f;
+        float a = 0.f;
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
           const int sidx = t + tap - KT / 2;
-          if (sidx >= 0 && sidx < TT) acc += l[sidx] * g[t];
+          if (sidx >= 0 && sidx < TT) a += l[sidx] * g[t];
         }
-        rr[M.sl.conv_k + tap * DT * DT + q] = acc;
+        RR_ADD(M.sl.conv_k, tap * DT * DT + q, a);
       }
     }
   } else {
@@ -1339,7 +1351,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
         const int sidx = t + tap - pad;
         if (sidx >= 0 && sidx < d.T) s += locs[sidx * d.D + ci] * dcv[t * d.D + co];
       }
-      rr[M.sl.conv_k + q] = s;
+      RR_ADD(M.sl.conv_k, q, s);
     }
   }
   if constexpr (DT > 0) {
@@ -1416,8 +1428,8 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
         s1 += p1[k * DT + tid];
         s2 += p2[k * DT + tid];
       }
-      rr[M.sl.loc_g + tid] = s1;
-      rr[M.sl.loc_b + tid] = s2;
+      RR_ADD(M.sl.loc_g, tid, s1);
+      RR_ADD(M.sl.loc_b, tid, s2);
     }
   } else {
   for (int e = tid; e < d.D; e += blockDim.x) {
@@ -1426,8 +1438,8 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
       s1 += dls[t * d.D + e] * M.a.loc_hat[rH + t * d.D + e];
       s2 += dls[t * d.D + e];
     }
-    rr[M.sl.loc_g + e] = s1;
-    rr[M.sl.loc_b + e] = s2;
+    RR_ADD(M.sl.loc_g, e, s1);
+    RR_ADD(M.sl.loc_b, e, s2);
   }
   for (int t = tid; t < d.T; t += blockDim.x) {
     float s1 = 0.f, s2 = 0.f;
@@ -1457,17 +1469,30 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     atomicAdd((unsigned long long*)&M.a.emb_acc[ctx[t] * d.D + e],
               (unsigned long long)emb_to_fixed(de + dxs[j]));
   }
+  __syncthreads();   // the next row reuses every smem row buffer
+  }   // rows of this CTA
+#undef RR_ADD
+  float* part = M.a.trunk_part + (long long)blockIdx.x * (M.sl.trunk1 - t0);
+  for (int c = tid; c < M.sl.trunk1 - t0; c += blockDim.x) part[c] = acc[c];
 }
 
 void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s) {
   const Dims& d = M.d;
   const size_t smem =
-      sizeof(float) * (4 * d.H + d.K * d.D * (d.D + 1) + 3 * d.D + 32) + sizeof(int) * d.T;
+      sizeof(float) * (4 * d.H + d.K * d.D * (d.D + 1) + 3 * d.D + 32) +
+      sizeof(int) * ((d.T + 3) & ~3) + sizeof(float) * (M.sl.trunk1 - M.sl.trunk0);
+  static const cudaError_t a1 = cudaFuncSetAttribute(
+      k_trunk_bwd<32, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  static const cudaError_t a2 = cudaFuncSetAttribute(
+      k_trunk_bwd<0, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  (void)a1;
+  (void)a2;
+  const dim3 grid(M.trunk_grid);
   if (d.D == 32 && d.T == 16 && d.K == 3)
-    launch_pdl(k_trunk_bwd<32, 16, 3>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
+    launch_pdl(k_trunk_bwd<32, 16, 3>, grid, dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
   else
-    launch_pdl(k_trunk_bwd<0, 0, 0>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
+    launch_pdl(k_trunk_bwd<0, 0, 0>, grid, dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
 }
 
 // Column sums of the per-row reduction buffer + dlogits (b_head), in a fixed
@@ -1507,14 +1532,18 @@ __global__ void __maxnreg__(40) k_small_adam(ModelPtrs M, int grad_only,
 #pragma unroll
   for (int k = 0; k < kColAcc; ++k) acc[k] = 0.f;
   if (c < total) {
-    const float* base = (c < R) ? M.a.rowred + c : M.a.dlogits + (c - R);
-    const long long ld = (c < R) ? R : kAlphabet;
+    // trunk_bwd's columns come as one partial row per trunk_bwd CTA
+    const bool trunk = c >= M.sl.trunk0 && c < M.sl.trunk1;
+    const float* base = trunk ? M.a.trunk_part + (c - M.sl.trunk0)
+                              : ((c < R) ? M.a.rowred + c : M.a.dlogits + (c - R));
+    const long long ld = trunk ? M.sl.trunk1 - M.sl.trunk0 : ((c < R) ? R : kAlphabet);
+    const int rows = trunk ? M.trunk_grid : M.d.B;
     int b = w;
-    for (; b + (kColAcc - 1) * kColWarps < M.d.B; b += kColAcc * kColWarps) {
+    for (; b + (kColAcc - 1) * kColWarps < rows; b += kColAcc * kColWarps) {
 #pragma unroll
       for (int k = 0; k < kColAcc; ++k) acc[k] += base[(long long)(b + k * kColWarps) * ld];
     }
-    for (; b < M.d.B; b += kColWarps) acc[0] += base[(long long)b * ld];
+    for (; b < rows; b += kColWarps) acc[0] += base[(long long)b * ld];
   }
   const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   part[w][lane] = s;

@@ -137,6 +137,25 @@ def test_bits_per_byte_default_1mib_within_half_percent():
     assert abs(rel) < 0.005, (ours, ref)
 
 
+@pytest.mark.parametrize("kind", ["dna", "mixed"])
+def test_bits_per_byte_default_1mib_dna_mixed(kind):
+    """Beyond criterion 5: the reference's own containers for 1 MiB of DNA and
+    mixed data at the default config (tests/golden/bpb_ref.jsonl, written by
+    tests/golden/make_bpb_ref.py running dszip, ~25 min each on the CPU)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_2604_07239_b200 import ModelConfig, container, corpus
+    recs = [json.loads(l) for l in open(os.path.join(GOLDEN, "bpb_ref.jsonl"))]
+    rec = next(r for r in recs if r["kind"] == kind)
+    data = getattr(corpus, "make_" + kind)(rec["n"], rec["seed"])
+    blob, _ = container.compress_bytes(data, ModelConfig(seed=5))
+    assert container.decompress_bytes(blob) == data
+    rel = (len(blob) - rec["bytes"]) / rec["bytes"]
+    print(f"default 1 MiB {kind}: ours {len(blob)} B vs reference {rec['bytes']} B ({100 * rel:+.3f}%)")
+    assert abs(rel) < 0.005, (len(blob), rec["bytes"])
+
+
 def test_sharded_v2_container_round_trip():
     """independent shards (here run one after another on one GPU),
     host-side gather into a v2 container, decode back bit-exactly."""

@@ -28,10 +28,12 @@ LN_EPS = 1e-5           # ops.py:16
 class TorchOracle:
     """Predictor.predict / train_step (model.py:183-215) on torch tensors."""
 
-    def __init__(self, cfg, device="cuda"):
+    def __init__(self, cfg, device="cuda", tf32=False):
         import torch
-        torch.backends.cuda.matmul.allow_tf32 = False
-        torch.backends.cudnn.allow_tf32 = False
+        # tf32=True is a diagnostic only: cuBLAS TF32 GEMMs (operands rounded
+        # to a 10-bit mantissa), to separate precision effects on long runs
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+        torch.backends.cudnn.allow_tf32 = tf32
         self.torch = torch
         self.cfg = cfg
         self.dev = device

@@ -1227,11 +1227,15 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   // [trunk0, trunk1) of the small arena (in_g ... w_val), accumulated over the
   // CTA's rows in row order and written once to trunk_part[blockIdx.x]; the
   // small-parameter kernel sums the gridDim.x partial rows in a fixed order
-  float* acc = (float*)(ctx + ((d.T + 3) & ~3));
+  // (one row per CTA -- B <= trunk grid -- writes its row straight to
+  // trunk_part; several rows accumulate in shared memory first)
+  const bool multi = d.B > (int)gridDim.x;
   const int t0 = M.sl.trunk0;
+  float* acc = multi ? (float*)(ctx + ((d.T + 3) & ~3))
+                     : M.a.trunk_part + (long long)blockIdx.x * (M.sl.trunk1 - t0);
   // rr[X + q] (a per-row column write of the CTA-per-row layout) becomes an
   // accumulate into this CTA's partial row; each column has one owner thread
-#define RR_ADD(off, q, v) (acc[(off) - t0 + (q)] += (v))
+#define RR_ADD(off, q, v) (multi ? (void)(acc[(off) - t0 + (q)] += (v)) : (void)(acc[(off) - t0 + (q)] = (v)))
   const float* Wg = M.w[P_W_GATE].p;
   const long long c0 = use_col ? M.st->col - d.T : 0;
   const float* Wv = M.w[P_W_VAL].p;
@@ -1243,12 +1247,12 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     const int tap = j / (d.D * d.D), ci = (j / d.D) % d.D, co = j % d.D;
     ck[(tap * d.D + co) * ckp + ci] = M.w[P_CONV_K].p[j];
   }
-  for (int c = tid; c < M.sl.trunk1 - t0; c += blockDim.x) acc[c] = 0.f;
+  if (multi)
+    for (int c = tid; c < M.sl.trunk1 - t0; c += blockDim.x) acc[c] = 0.f;
   const VFlags vf = vflags(M.variant);
   for (int b = blockIdx.x; b < d.B; b += gridDim.x) {
   const long long rH = (long long)b * d.H;
   for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
-  __syncthreads();
   if (vf.global) {
     for (int o = tid; o < d.D; o += blockDim.x) {
       const float gp = M.a.gpre[(long long)b * d.D + o];
@@ -1469,19 +1473,22 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     atomicAdd((unsigned long long*)&M.a.emb_acc[ctx[t] * d.D + e],
               (unsigned long long)emb_to_fixed(de + dxs[j]));
   }
-  __syncthreads();   // the next row reuses every smem row buffer
+  if (multi) __syncthreads();   // the next row reuses every smem row buffer
   }   // rows of this CTA
 #undef RR_ADD
-  float* part = M.a.trunk_part + (long long)blockIdx.x * (M.sl.trunk1 - t0);
-  for (int c = tid; c < M.sl.trunk1 - t0; c += blockDim.x) part[c] = acc[c];
+  if (multi) {
+    float* part = M.a.trunk_part + (long long)blockIdx.x * (M.sl.trunk1 - t0);
+    for (int c = tid; c < M.sl.trunk1 - t0; c += blockDim.x) part[c] = acc[c];
+  }
 }
 
 void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s) {
   const Dims& d = M.d;
+  const bool multi = d.B > M.trunk_grid;
   const size_t smem =
       sizeof(float) * (4 * d.H + d.K * d.D * (d.D + 1) + 3 * d.D + 32) +
-      sizeof(int) * ((d.T + 3) & ~3) + sizeof(float) * (M.sl.trunk1 - M.sl.trunk0);
+      sizeof(int) * ((d.T + 3) & ~3) + (multi ? sizeof(float) * (M.sl.trunk1 - M.sl.trunk0) : 0);
   static const cudaError_t a1 = cudaFuncSetAttribute(
       k_trunk_bwd<32, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   static const cudaError_t a2 = cudaFuncSetAttribute(

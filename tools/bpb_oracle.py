@@ -53,7 +53,7 @@ def quantize_t(p):
     return torch.clamp(v, min=1)
 
 
-def oracle_run(data, cfg):
+def oracle_run(data, cfg, tf32=False):
     import numpy as np
     import torch
     from oracle.torch_model import TorchOracle
@@ -64,7 +64,7 @@ def oracle_run(data, cfg):
     T = cfg.ctx_len
     warm = min(T, L)
     dmat = torch.from_numpy(np.ascontiguousarray(mat)).cuda().long()
-    m = TorchOracle(cfg)
+    m = TorchOracle(cfg, tf32=tf32)
     bits = torch.zeros((), dtype=torch.float64, device="cuda")
     qbits = torch.zeros((), dtype=torch.float64, device="cuda")
     losses = torch.zeros(max(L - warm, 1), dtype=torch.float64, device="cuda")
@@ -88,6 +88,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("workloads", nargs="+", help="kind:n:seed")
     ap.add_argument("--gpu", action="store_true", help="also compress with this package")
+    ap.add_argument("--tf32", action="store_true",
+                    help="diagnostic: the oracle's GEMMs on TF32 tensor cores instead of fp32")
     a = ap.parse_args()
     from paper_2604_07239_b200 import ModelConfig, container, corpus
     for spec in a.workloads:
@@ -95,8 +97,9 @@ def main():
         data = getattr(corpus, "make_" + kind)(int(n), int(seed))
         cfg = ModelConfig(seed=5).shrink_to_fit(len(data))
         t0 = time.perf_counter()
-        est, ideal, mean_loss, steps = oracle_run(data, cfg)
+        est, ideal, mean_loss, steps = oracle_run(data, cfg, a.tf32)
         rec = {"workload": f"make_{kind}({n}, {seed}), ModelConfig(seed=5)", "steps": steps,
+               "oracle_gemms": "tf32" if a.tf32 else "fp32",
                "oracle_bytes_est": est, "oracle_bpb_est": 8.0 * est / len(data),
                "oracle_bytes_unquantised": ideal,
                "oracle_mean_loss_nats": mean_loss, "oracle_s": time.perf_counter() - t0}

@@ -352,7 +352,7 @@ def run_ours(args):
         ach, peak, unit = kk["flops"] / (kk["ms"] / 1e3) / 1e12, tf32, "TFLOP/s"
     # DRAM traffic per launch from the committed ncu capture of that component
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")
     if os.path.exists(tpath):
         t = json.load(open(tpath)).get(top)
         if t:

@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu --nvtx
+
 #include "../../include/fade_b200.h"
 #include "model.cuh"
 #include "stream_coder.cuh"
@@ -879,6 +881,16 @@ static int replay_live(fade_model* m) {
   return FADE_OK;
 }
 
+// NVTX range over a scope (profiler ranges per phase of
+// the executors -- upload, warm-up coding, graph capture, the replayed
+// timesteps, flush / decode fetch); free when no tool is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // runs a callable when the scope exits (every error path included)
 template <class F>
 struct Defer {
@@ -902,13 +914,17 @@ static int replay_steps(fade_model_t* m, long long n, unsigned long long* tape, 
     if (graph) cudaGraphDestroy(graph);
   });
   m->M.tape = tape;
-  CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
-  const int status = body();
-  const cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
-  m->M.tape = nullptr;
-  if (status != FADE_OK) return status;
-  CK(ce);
-  CK(cudaGraphInstantiate(&exec, graph, 0));
+  {
+    NvtxRange r("fade: capture timestep graph");
+    CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
+    const int status = body();
+    const cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
+    m->M.tape = nullptr;
+    if (status != FADE_OK) return status;
+    CK(ce);
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  NvtxRange r("fade: timesteps (graph replays)");
   for (long long i = 0; i < n; ++i) CK(cudaGraphLaunch(exec, m->s_main));
   CK(cudaStreamSynchronize(m->s_main));
   return FADE_OK;
@@ -1406,8 +1422,10 @@ int fade_compress(fade_model_t* m, int device, int batch, const uint8_t* data, i
     dev_free(dtape, s);
     cudaStreamSynchronize(s);
   });
+  NvtxRange range("fade_compress");
   const uint8_t* mat = data;
   if (!on_device && nbytes) {
+    NvtxRange r("fade: upload stream matrix");
     CK(dev_alloc((void**)&dmat, nbytes, s));
     CK(cudaMemcpyAsync(dmat, data, nbytes, cudaMemcpyHostToDevice, s));
     mat = dmat;
@@ -1442,6 +1460,7 @@ int fade_compress(fade_model_t* m, int device, int batch, const uint8_t* data, i
       CK(cudaMemcpy(tape, dtape, sizeof(unsigned long long) * kTapeSlots * (size_t)nsteps,
                     cudaMemcpyDeviceToHost));
   }
+  NvtxRange rf("fade: flush + lengths");
   launch_encode_flush(c->e, batch, s);
   c->lengths.resize(batch);
   CK(cudaMemcpyAsync(c->lengths.data(), c->e.blen, sizeof(long long) * batch,
@@ -1516,6 +1535,7 @@ int fade_decompress(fade_model_t* m, int device, int batch, const uint8_t* paylo
     unsigned long long none = ~0ull;
     CK(cudaMemcpyAsync(err_key, &none, 8, cudaMemcpyHostToDevice, s));
   }
+  NvtxRange range("fade_decompress");
   launch_dec_prime(ds, batch, err_key, s);
   launch_decode_warm(ds, batch, dmat, L, warm, err_key, s);
   if (m && nsteps > 0) {

@@ -207,3 +207,25 @@ def test_metrics_tape_router_stats():
     assert out == data
     assert [(r["loss_nats"], r["alpha_mean"], r["alpha_min"], r["alpha_max"]) for r in dtape] == \
         [(r["loss_nats"], r["alpha_mean"], r["alpha_min"], r["alpha_max"]) for r in tape]
+
+
+def test_file_helpers_and_metrics_jsonl(tmp_path):
+    """container.compress_file / decompress_file / inspect_file (the CLI's
+    backing calls, container.py:186-220): report keys, lossless files, and the
+    --metrics JSONL tape with device-clock elapsed_s."""
+    import json
+    from paper_2604_07239_b200 import container, corpus
+    data = corpus.make_text(5000, 2)
+    src, dst, back, met = (tmp_path / n for n in ("in", "out.fade", "back", "m.jsonl"))
+    src.write_bytes(data)
+    rep = container.compress_file(src, dst, tiny(), metrics_path=met)
+    assert {"original_bytes", "compressed_bytes", "ratio", "bits_per_byte", "seconds",
+            "kb_per_min", "n_streams", "pipelined"} <= set(rep)
+    assert rep["compressed_bytes"] == dst.stat().st_size
+    recs = [json.loads(l) for l in met.read_text().splitlines()]
+    assert recs and all(r["phase"] == "compress" for r in recs)
+    assert all(b["elapsed_s"] > a["elapsed_s"] for a, b in zip(recs, recs[1:]))
+    rep2 = container.decompress_file(dst, back)
+    assert back.read_bytes() == data and rep2["original_bytes"] == len(data)
+    info = container.inspect_file(dst)
+    assert info["version"] == 1 and info["checksums_ok"] and info["original_length"] == len(data)

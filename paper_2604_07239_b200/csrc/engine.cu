@@ -522,9 +522,16 @@ static int allocate(fade_model* m) {
   // split-K factors sized to ~one wave of 148 SMs (kWideBN tiles)
   const int tiles = cdiv(B, kBM) * cdiv(H, kWideBN);
   M.splits_mem = choose_splits(tiles, cdiv(C, kBK));
-  M.splits_f = choose_splits(tiles, cdiv(d.E, kBK));
+  // F and dz2 capped: below B = 512 one wave of slices writes as many
+  // partial-plane bytes as the GEMM reads weight bytes, and the row kernel
+  // after it reads them all back (B = 64 / 128 / 256, F: 74 / 74 / 37 slices
+  // -> 18 and dz2 74 / 74 / 37 -> 36 / 36 / 18: -6 / -18 / -4 us per
+  // timestep; B = 512 keeps 18 / 18)
+  M.splits_f = std::min(choose_splits(tiles, cdiv(d.E, kBK)), 18);
   if (const char* e = knob("FADE_SPLITS_F")) M.splits_f = std::max(1, atoi(e));   // experiments
-  M.splits_dz2 = choose_splits(tiles, cdiv(2 * Ep, kBK));
+  M.splits_dz2 = std::min(choose_splits(tiles, cdiv(2 * Ep, kBK)), B <= 128 ? 36 : 18);
+  if (const char* e = knob("FADE_SPLITS_MEM")) M.splits_mem = std::max(1, atoi(e));   // experiments
+  if (const char* e = knob("FADE_SPLITS_DZ2")) M.splits_dz2 = std::max(1, atoi(e));   // experiments
   // Only the forward's narrow GEMMs split: in the backward the side stream's
   // weight updates hold most SMs, and a 128-CTA input-gradient GEMM waits for
   // slots an 8-40-CTA one slips into (measured: each backward split +2-7 us

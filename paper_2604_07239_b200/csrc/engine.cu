@@ -326,6 +326,14 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
                                                    : (1L << G_WROUTE_WMEM);
   for (int id = 0; id < G_COUNT; ++id)
     if ((bn64_ids >> id) & 1) m->bn[id] = 64;
+  // B <= 128: the expand GEMM at 128-wide single-CTA tiles (150 tiles over
+  // 148 persistent CTAs instead of 75 pair tiles over 74 pairs: the one
+  // doubled unit is half as long): -3 us per timestep at B = 64 / 128,
+  // +4 / +8 us at B = 256 / 512
+  if (M.d.B <= 128) m->bn[G_E12] = 128;
+  static const long bn128_ids = knob("FADE_BN128") ? atol(knob("FADE_BN128")) : 0;   // experiments
+  for (int id = 0; id < G_COUNT; ++id)
+    if ((bn128_ids >> id) & 1) m->bn[id] = 128;
   // CTA pairs (cta_group::2, 256-row tiles): half the operand bytes per SM
   // (W12 update, the GeGLU backward and dz2: -15 us per step together; the
   // FNR project GEMM F (split-K 18, 144 CTAs): -1.7 us;

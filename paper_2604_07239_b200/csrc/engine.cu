@@ -99,6 +99,8 @@ struct fade_model {
   SmallLayout sl;
   int device = 0;
   cudaStream_t s_main = nullptr, s_side = nullptr, s_coder = nullptr;
+  cudaStream_t s_side2 = nullptr;   // second weight-update stream (side2_mask)
+  cudaEvent_t ev_side2_done = nullptr;
   cudaEvent_t ev[8] = {};
   cudaEvent_t ev_cum[2] = {}, ev_enc[2] = {}, ev_side_done = nullptr, ev_coder_join = nullptr;
   cudaEvent_t ev_wu[2] = {};    // W_U update forked off the model stream (experiments)
@@ -513,8 +515,8 @@ static int run_gemm(fade_model* m, int id, cudaStream_t s, bool grad_only = fals
     std::call_once(warned, [] {
       fprintf(stderr, "[fade] FADE_DBG_SKIP/FADE_DBG_SKIPID set: GEMMs are skipped, results are invalid\n");
     });
-  if ((dbg_skip & 1) && s == m->s_side) return FADE_OK;
-  if ((dbg_skip & 2) && s != m->s_side) return FADE_OK;
+  if ((dbg_skip & 1) && (s == m->s_side || s == m->s_side2)) return FADE_OK;
+  if ((dbg_skip & 2) && s != m->s_side && s != m->s_side2) return FADE_OK;
   if (dbg_ids & (1L << id)) return FADE_OK;
 #endif
   return gemm_launch(grad_only ? m->Gg[id] : m->G[id], m->bn[id], s);
@@ -719,9 +721,9 @@ static int forward(fade_model* m, const StepIO& io, bool with_head) {
 }
 
 // fork the side stream off the model stream at this point
-static int fork_side(fade_model* m, int k) {
+static int fork_side(fade_model* m, int k, cudaStream_t side) {
   CK(cudaEventRecord(m->ev[k], m->s_main));
-  CK(cudaStreamWaitEvent(m->s_side, m->ev[k], 0));
+  CK(cudaStreamWaitEvent(side, m->ev[k], 0));
   return FADE_OK;
 }
 
@@ -744,14 +746,26 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
     return a;
   }();
   const int ids[4] = {G_WF, G_W12, G_WUP_WCGATE, G_WROUTE_WMEM};
+  // bit k of side2_mask puts update ids[k] on a second side stream, where it
+  // overlaps the other updates instead of queueing behind them.  B <= 256:
+  // the W_route/W_mem update (the step's last kernel: the side stream, not
+  // the model stream, ends a small-B step) -9 / -11 / -4 us per timestep at
+  // B = 64 / 128 / 256; B = 512: +10 us (it then competes with trunk_bwd).
+  // Experiments: FADE_SIDE2 = mask.
+  static const int side2_env = knob("FADE_SIDE2") ? atoi(knob("FADE_SIDE2")) : -1;
+  const int side2_mask = side2_env >= 0 ? side2_env : (M.d.B <= 256 ? 8 : 0);
+  bool used2 = false;
   int pos = 0;
   auto sides = [&]() -> int {
-    bool forked = false;
+    bool forked[2] = {false, false};
     for (int k = 0; k < 4; ++k) {
       if (at[k] != pos) continue;
-      if (!forked) TRY(fork_side(m, pos % 8));
-      forked = true;
-      TRY(run_gemm(m, ids[k], side, grad_only));
+      const int j = (side2_mask >> k) & 1;
+      cudaStream_t ss = j ? m->s_side2 : side;
+      if (!forked[j]) TRY(fork_side(m, pos % 8, ss));
+      forked[j] = true;
+      used2 |= j != 0;
+      TRY(run_gemm(m, ids[k], ss, grad_only));
     }
     ++pos;
     return FADE_OK;
@@ -804,6 +818,10 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   launch_small_adam(M, grad_only, losses, io.alpha_tape, advance, s);
   CK(cudaEventRecord(m->ev_side_done, side));
   CK(cudaStreamWaitEvent(s, m->ev_side_done, 0));
+  if (used2) {
+    CK(cudaEventRecord(m->ev_side2_done, m->s_side2));
+    CK(cudaStreamWaitEvent(s, m->ev_side2_done, 0));
+  }
   if (wu_forked) CK(cudaStreamWaitEvent(s, m->ev_wu[1], 0));
   CK(cudaGetLastError());
   return FADE_OK;
@@ -986,6 +1004,8 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   if (!dbg_prio) prio_hi = prio_lo;
   CK(cudaStreamCreateWithPriority(&m->s_main, cudaStreamNonBlocking, prio_hi));
   CK(cudaStreamCreateWithPriority(&m->s_side, cudaStreamNonBlocking, prio_lo));
+  CK(cudaStreamCreateWithPriority(&m->s_side2, cudaStreamNonBlocking, prio_lo));
+  CK(cudaEventCreateWithFlags(&m->ev_side2_done, cudaEventDisableTiming));
   CK(cudaStreamCreateWithPriority(&m->s_coder, cudaStreamNonBlocking, prio_hi));
   for (auto& e : m->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
@@ -1030,10 +1050,12 @@ int fade_model_destroy(fade_model_t* m) {
     cudaEventDestroy(m->ev_enc[i]);
   }
   cudaEventDestroy(m->ev_side_done);
+  cudaEventDestroy(m->ev_side2_done);
   cudaEventDestroy(m->ev_coder_join);
   for (auto& e : m->ev_wu) cudaEventDestroy(e);
   cudaStreamDestroy(m->s_main);
   cudaStreamDestroy(m->s_side);
+  cudaStreamDestroy(m->s_side2);
   cudaStreamDestroy(m->s_coder);
   delete m;
   return FADE_OK;

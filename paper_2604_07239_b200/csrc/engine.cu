@@ -110,6 +110,8 @@ struct fade_model {
   GemmParams G[G_COUNT];        // step schedule (Adam fused into dW epilogues)
   GemmParams Gg[G_COUNT];       // loss_grads variant (dW epilogues store gradients)
   int bn[G_COUNT];
+  const uint8_t* bench_src = nullptr;   // last fade_bench_compress_steps input (probe)
+  long long bench_L = 0;
   uint8_t* ctx_buf = nullptr;   // [B][T]  (predict API)
   uint8_t* tgt_buf = nullptr;   // [B]
   double* loss_buf = nullptr;   // [1]
@@ -540,6 +542,7 @@ static int allocate(fade_model* m) {
   M.splits_f = std::min(choose_splits(tiles, cdiv(d.E, kBK)), 18);
   if (const char* e = knob("FADE_SPLITS_F")) M.splits_f = std::max(1, atoi(e));   // experiments
   M.splits_dz2 = std::min(choose_splits(tiles, cdiv(2 * Ep, kBK)), B <= 128 ? 36 : 18);
+  if (const char* e = knob("FADE_DBG_TRUNK")) M.dbg = atoi(e);   // experiments (invalid results)
   if (const char* e = knob("FADE_SPLITS_MEM")) M.splits_mem = std::max(1, atoi(e));   // experiments
   if (const char* e = knob("FADE_SPLITS_DZ2")) M.splits_dz2 = std::max(1, atoi(e));   // experiments
   // Only the forward's narrow GEMMs split: in the backward the side stream's
@@ -1645,6 +1648,13 @@ int fade_bench_probe(fade_model_t* m, int which, int iters, double* ms, double* 
   ON_DEVICE(m->device);
   const Dims& d = m->d;
   const double B = d.B, H = d.H, Ep = d.Ep, C = d.C, X = d.X;
+  // trunk kernels: the context window of the last fade_bench_compress_steps
+  // call (real data: the embedding-gradient atomics contend as in a step)
+  if (which >= 5 && !m->bench_src) {
+    set_last_error("bench_probe: run fade_bench_compress_steps first");
+    return FADE_ERR_USAGE;
+  }
+  const uint8_t* probe_src = m->bench_src;
   auto launch = [&]() -> int {
     switch (which) {
       case 0: return run_gemm(m, G_E12, m->s_main);
@@ -1652,6 +1662,9 @@ int fade_bench_probe(fade_model_t* m, int which, int iters, double* ms, double* 
       case 2: return run_gemm(m, G_WROUTE_WMEM, m->s_main);
       case 3: launch_bmm_bwd(m->M, 0, 3, m->s_main); return FADE_OK;
       case 4: return run_gemm(m, G_F, m->s_main);
+      case 5: launch_trunk_bwd(m->M, probe_src, m->bench_L, 1, m->s_main); return FADE_OK;
+      case 6: launch_trunk_fwd(m->M, probe_src, m->bench_L, 1, m->s_main); return FADE_OK;
+      case 7: launch_small_adam(m->M, 0, nullptr, nullptr, 0, m->s_main); return FADE_OK;
     }
     set_last_error("bench_probe: unknown component");
     return FADE_ERR_USAGE;
@@ -1678,6 +1691,10 @@ int fade_bench_probe(fade_model_t* m, int which, int iters, double* ms, double* 
       *flops = 2.0 * B * d.E * H;
       *bytes = 4.0 * (d.E * H + B * Ep + (double)m->M.splits_f * B * H);
       break;
+    default:   // trunk_bwd / trunk_fwd / small_adam: latency, not bytes
+      *flops = 0.0;
+      *bytes = 0.0;
+      break;
   }
   TRY(launch());   // warm
   cudaEvent_t e0, e1;
@@ -1699,6 +1716,8 @@ int fade_bench_compress_steps(fade_model_t* m, const uint8_t* data_dev, int64_t 
                               int64_t steps, fade_coder_t** coder, int* launches, void* stream) {
   (void)stream;
   ON_DEVICE(m->device);
+  m->bench_src = data_dev;
+  m->bench_L = L;
   if (!*coder) {
     TRY(coder_create(m->d.B, L, m->device, m->s_main, coder));
     TRY(set_col(m, start, start));

@@ -138,6 +138,7 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   // trunk_bwd grid: min(B, 4 per SM); each CTA loops over rows b = cta,
   // cta + grid, ... and writes one partial row of its small-parameter sums
   int trunk_grid;
+  int dbg;   // experiments build only (FADE_DBG_TRUNK): bit 0 drops the embedding-gradient atomics
 };
 __device__ __forceinline__ unsigned long long* tape_at(const ModelPtrs& M, int slot) {
   return M.tape + kTapeSlots * (M.st->col - M.st->loss_base) + slot;
@@ -150,6 +151,8 @@ bool launch_out_fwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_out_bwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_coarse_bwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_mix_bwd_w(const ModelPtrs& M, cudaStream_t s);
+bool launch_trunk_fwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                        cudaStream_t s);
 bool row_warp_enabled(int B, int which);   // which: 0 mix_fwd .. 5 mix_bwd
 
 // row kernels (model_kernels.cu)

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   pdl_enter();
   Dims d = M.d;
   if (DT) { d.D = DT; d.T = TT; d.K = KT; d.H = DT * TT; }
-  const int b = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   extern __shared__ float sm[];
   float* es = sm;                         // raw embedding row [H]
   float* xs = es + d.H;                   // x row [H]
@@ -158,8 +158,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
 
   const VFlags vf = vflags(M.variant);
   const long long c0 = use_col ? M.st->col - d.T : 0;
-  if (M.tape && b == 0 && tid == 0) *tape_at(M, 0) = gtimer_ns();
-  float* crow = M.a.cache + (long long)b * d.C;
+  if (M.tape && blockIdx.x == 0 && tid == 0) *tape_at(M, 0) = gtimer_ns();
   const int n4 = (d.C - d.D) / 4;        // float4 count the roll moves
   // ring buffer (block-major [C/32][B][32], model.cuh): the new block
   // overwrites the oldest one in place; nothing else moves (ref
@@ -168,22 +167,9 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   const bool ring = M.ring_on;
   const int rnb = d.C / 32, rstep = d.D / 32;
   const int rb0 = ring ? (int)((M.st->ring * rstep) % rnb) : 0;
-  auto ring_elem = [&](int o) -> float* {
-    return M.a.cache + (((long long)((rb0 + (o >> 5)) % rnb) * d.B + b) << 5) + (o & 31);
-  };
-  if constexpr (DT > 0) {
-    // the roll's reads depend on nothing this kernel computes: start them
-    // first (cp.async into smem) so they land under the LayerNorm/GeGLU work
-    if (vf.global && !ring) {
-      for (int q = tid; q < n4; q += blockDim.x)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(cstage + 4 * q)),
-                     "l"(crow + d.D + 4 * q)
-                     : "memory");
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-  }
-  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
+  // the weights are staged once per CTA; a CTA walks rows b = cta, cta +
+  // grid, ... (grid = min(B, 4 per SM): at large B the 20 KB of weights are
+  // not re-read for every row)
   if constexpr (DT > 0) {
     // weights into smem as float4: at the compiled geometry (D = 32, H = 512)
     // every small-arena offset is a multiple of 4 floats (make_small_layout)
@@ -211,6 +197,24 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     }
     for (int j = tid; j < d.K * d.D * d.D; j += blockDim.x) ck[j] = M.w[P_CONV_K].p[j];
   }
+  for (int b = blockIdx.x; b < d.B; b += gridDim.x) {
+  float* crow = M.a.cache + (long long)b * d.C;
+  auto ring_elem = [&](int o) -> float* {
+    return M.a.cache + (((long long)((rb0 + (o >> 5)) % rnb) * d.B + b) << 5) + (o & 31);
+  };
+  if constexpr (DT > 0) {
+    // the roll's reads depend on nothing this kernel computes: start them
+    // first (cp.async into smem) so they land under the LayerNorm/GeGLU work
+    if (vf.global && !ring) {
+      for (int q = tid; q < n4; q += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(cstage + 4 * q)),
+                     "l"(crow + d.D + 4 * q)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  }
+  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
   __syncthreads();
 
   // embedding gather + input LayerNorm over the flattened window
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     for (int o = tid; o < d.D; o += blockDim.x) crow[d.C - d.D + o] = blk[o];
   }
   }   // global stream
-  if (!vf.local) return;
+  if (vf.local) {
 
   // local stream: per-symbol LayerNorm over D (ops.py:94-101 on (B,T,D))
   if constexpr (DT > 0) {
@@ -384,8 +388,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     M.a.h_l[rH + t0 * DT + co] = gelu_f(acc0);
     M.a.conv_pre[rH + t1 * DT + co] = acc1;
     M.a.h_l[rH + t1 * DT + co] = gelu_f(acc1);
-    return;
-  }
+  } else {
   for (int j = tid; j < d.H; j += blockDim.x) {
     const int t = j / d.D, co = j % d.D;
     float acc = cb[co];
@@ -401,11 +404,16 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
     M.a.conv_pre[rH + j] = acc;
     M.a.h_l[rH + j] = gelu_f(acc);
   }
+  }
+  }   // local stream
+  __syncthreads();   // the next row reuses every smem row buffer
+  }   // rows of this CTA
 }
 
 void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s) {
   const Dims& d = M.d;
+  if (row_warp_enabled(d.B, 6) && launch_trunk_fwd_w(M, src, ld_src, use_col, s)) return;
   const size_t smem = sizeof(float) * (3 * d.H + (2 + d.K) * d.D * d.D + d.D + 2 * d.T + 32) +
                       sizeof(int) * d.T;
   // + the staged cache tail when the cache rolls (a ring buffer moves nothing)
@@ -414,10 +422,11 @@ void launch_trunk_fwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
     static const cudaError_t attr = cudaFuncSetAttribute(
         k_trunk_fwd<32, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 1024);
     (void)attr;
-    launch_pdl(k_trunk_fwd<32, 16, 3>, dim3(d.B), dim3(kTrunkThreads), smem_dt, s, M, src, ld_src,
-               use_col);
+    launch_pdl(k_trunk_fwd<32, 16, 3>, dim3(M.trunk_grid), dim3(kTrunkThreads), smem_dt, s, M, src,
+               ld_src, use_col);
   } else {
-    launch_pdl(k_trunk_fwd<0, 0, 0>, dim3(d.B), dim3(kTrunkThreads), smem, s, M, src, ld_src, use_col);
+    launch_pdl(k_trunk_fwd<0, 0, 0>, dim3(M.trunk_grid), dim3(kTrunkThreads), smem, s, M, src, ld_src,
+               use_col);
   }
 }
 
@@ -1222,7 +1231,10 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   float* dv = dg + d.D;                   // [D] dvpre
   float* xt = dv + d.D;                   // [D]
   float* red = xt + d.D;                  // [32]
-  int* ctx = (int*)(red + 32);            // [T] context symbols
+  float* xh = red + 32;                   // [H] x_hat (input LayerNorm)
+  float* lhs = xh + d.H;                  // [H] loc_hat (per-symbol LayerNorm)
+  float* lis = lhs + d.H;                 // [T] loc_inv
+  int* ctx = (int*)(lis + ((d.T + 3) & ~3));   // [T] context symbols
   // per-CTA sums of this kernel's small-parameter gradient columns
   // [trunk0, trunk1) of the small arena (in_g ... w_val), accumulated over the
   // CTA's rows in row order and written once to trunk_part[blockIdx.x]; the
@@ -1252,7 +1264,14 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   const VFlags vf = vflags(M.variant);
   for (int b = blockIdx.x; b < d.B; b += gridDim.x) {
   const long long rH = (long long)b * d.H;
-  for (int t = tid; t < d.T; t += blockDim.x) ctx[t] = src[(long long)b * ld_src + c0 + t];
+  // every global input of the row is loaded in this one round (the
+  // LayerNorm phases below read x_hat / loc_hat / loc_inv from shared
+  // memory instead of a dependent global round each)
+  const float xinv = M.a.x_inv[b];
+  for (int t = tid; t < d.T; t += blockDim.x) {
+    ctx[t] = src[(long long)b * ld_src + c0 + t];
+    if (vf.local) lis[t] = M.a.loc_inv[(long long)b * d.T + t];
+  }
   if (vf.global) {
     for (int o = tid; o < d.D; o += blockDim.x) {
       const float gp = M.a.gpre[(long long)b * d.D + o];
@@ -1269,9 +1288,11 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     if (vf.router) dx = sk_sum(M.sk[S_DXR], (long long)d.B * d.H, rH + j);
     if (vf.global) dx = vf.router ? dx + M.a.dx_part[rH + j] : M.a.dx_part[rH + j];
     dxs[j] = dx;
+    xh[j] = M.a.x_hat[rH + j];
     if (vf.local) {
       dcv[j] = M.a.dh_l[rH + j] * gelu_grad_f(M.a.conv_pre[rH + j]);
       locs[j] = M.a.loc[rH + j];
+      lhs[j] = M.a.loc_hat[rH + j];
     }
   }
   __syncthreads();
@@ -1309,14 +1330,13 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   // input LayerNorm backward
   const float* gin = M.w[P_IN_LN_G].p;
   for (int j = tid; j < d.H; j += blockDim.x) {
-    RR_ADD(M.sl.in_g, j, dxs[j] * M.a.x_hat[rH + j]);
+    RR_ADD(M.sl.in_g, j, dxs[j] * xh[j]);
     RR_ADD(M.sl.in_b, j, dxs[j]);
   }
   float m1, m2;
-  ln_bwd_means(dxs, M.a.x_hat + rH, gin, d.H, red, &m1, &m2);
-  const float xinv = M.a.x_inv[b];
+  ln_bwd_means(dxs, xh, gin, d.H, red, &m1, &m2);
   for (int j = tid; j < d.H; j += blockDim.x)
-    dxs[j] = (dxs[j] * gin[j] - m1 - M.a.x_hat[rH + j] * m2) * xinv;   // dxf
+    dxs[j] = (dxs[j] * gin[j] - m1 - xh[j] * m2) * xinv;   // dxf
   if (vf.local) {
   // conv gradients: bias, taps, input (ops.py:74-88)
   const int pad = d.K / 2;
@@ -1412,7 +1432,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
 #pragma unroll
     for (int t = w; t < TT; t += 8) {
       const float dl = dls[t * DT + e];
-      const float lh = M.a.loc_hat[rH + t * DT + e];
+      const float lh = lhs[t * DT + e];
       q1 += dl * lh;
       q2 += dl;
       const float gg = dl * lg[e];
@@ -1439,7 +1459,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
   for (int e = tid; e < d.D; e += blockDim.x) {
     float s1 = 0.f, s2 = 0.f;
     for (int t = 0; t < d.T; ++t) {
-      s1 += dls[t * d.D + e] * M.a.loc_hat[rH + t * d.D + e];
+      s1 += dls[t * d.D + e] * lhs[t * d.D + e];
       s2 += dls[t * d.D + e];
     }
     RR_ADD(M.sl.loc_g, e, s1);
@@ -1450,7 +1470,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     for (int e = 0; e < d.D; ++e) {
       const float gg = dls[t * d.D + e] * lg[e];
       s1 += gg;
-      s2 += gg * M.a.loc_hat[rH + t * d.D + e];
+      s2 += gg * lhs[t * d.D + e];
     }
     // stash per-t means in the tail of locs (no longer needed after dloc)
     locs[2 * t] = s1 / (float)d.D;
@@ -1464,14 +1484,13 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
     const int t = j / d.D, e = j % d.D;
     float de = 0.f;
     if (vf.local) {
-      const float lh = M.a.loc_hat[rH + j];
-      de = (dls[j] * lg[e] - locs[2 * t] - lh * locs[2 * t + 1]) *
-           M.a.loc_inv[(long long)b * d.T + t];
+      de = (dls[j] * lg[e] - locs[2 * t] - lhs[j] * locs[2 * t + 1]) * lis[t];
     }
     // embedding gradient (ops.py:234-243 scatter-add): integer adds commute,
     // so the fixed-point sum is the same whatever order the rows arrive in
-    atomicAdd((unsigned long long*)&M.a.emb_acc[ctx[t] * d.D + e],
-              (unsigned long long)emb_to_fixed(de + dxs[j]));
+    if (!(M.dbg & 1))
+      atomicAdd((unsigned long long*)&M.a.emb_acc[ctx[t] * d.D + e],
+                (unsigned long long)emb_to_fixed(de + dxs[j]));
   }
   if (multi) __syncthreads();   // the next row reuses every smem row buffer
   }   // rows of this CTA
@@ -1487,7 +1506,7 @@ void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, 
   const Dims& d = M.d;
   const bool multi = d.B > M.trunk_grid;
   const size_t smem =
-      sizeof(float) * (4 * d.H + d.K * d.D * (d.D + 1) + 3 * d.D + 32) +
+      sizeof(float) * (6 * d.H + d.K * d.D * (d.D + 1) + 3 * d.D + 32 + ((d.T + 3) & ~3)) +
       sizeof(int) * ((d.T + 3) & ~3) + (multi ? sizeof(float) * (M.sl.trunk1 - M.sl.trunk0) : 0);
   static const cudaError_t a1 = cudaFuncSetAttribute(
       k_trunk_bwd<32, 16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);

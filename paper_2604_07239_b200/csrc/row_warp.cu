@@ -440,6 +440,180 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_mix_bwd_w(ModelPtrs M) {
 }
 
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// trunk + local stream forward, warp per row (model.py:118-137; the
+// compiled geometry D = 32, T = 16, K = 3 only, rolling cache not a ring).
+// Lane e holds column e of every context symbol t (es[t] = emb[ctx[t]][e]),
+// so the input LayerNorm, the per-symbol LayerNorm and the GeGLU block are
+// warp butterflies / shuffles, and the conv runs lane = output channel over
+// the warp's normalised window staged in shared memory (float4 broadcasts).
+// The weights are staged once per CTA; warps walk rows b = warp id,
+// + grid warps, ...  Same semantics as k_trunk_fwd<32, 16, 3>; only the
+// summation order of its reductions differs.
+constexpr int kTfWarps = 8;
+constexpr int kTfD = 32, kTfT = 16, kTfK = 3, kTfH = kTfD * kTfT;
+constexpr int kTfSmemFloats = 2 * kTfD * kTfD + kTfK * kTfD * kTfD + kTfWarps * kTfH;
+
+__global__ void __launch_bounds__(32 * kTfWarps, 2) k_trunk_fwd_w(ModelPtrs M, const uint8_t* src,
+                                                                 long long ld_src, int use_col) {
+  pdl_enter();
+  extern __shared__ float4 tf_sm4[];
+  float* wg = (float*)tf_sm4;                 // [D][D]   W_gate
+  float* wv = wg + kTfD * kTfD;               // [D][D]   W_val
+  float* ck = wv + kTfD * kTfD;               // [K][D][D] conv taps [tap][ci][co]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  float* locw = ck + kTfK * kTfD * kTfD + w * kTfH;   // this warp's normalised window
+  const VFlags vf = vflags(M.variant);
+  const Dims& d = M.d;
+  const long long c0 = use_col ? M.st->col - kTfT : 0;
+  if (M.tape && blockIdx.x == 0 && tid == 0) *tape_at(M, 0) = gtimer_ns();
+  {
+    const float4* g4 = (const float4*)M.w[P_W_GATE].p;
+    const float4* v4 = (const float4*)M.w[P_W_VAL].p;
+    const float4* k4 = (const float4*)M.w[P_CONV_K].p;
+    float4* s4 = tf_sm4;
+    for (int j = tid; j < kTfD * kTfD / 4; j += blockDim.x) {
+      s4[j] = g4[j];
+      s4[kTfD * kTfD / 4 + j] = v4[j];
+    }
+    for (int j = tid; j < kTfK * kTfD * kTfD / 4; j += blockDim.x) s4[kTfD * kTfD / 2 + j] = k4[j];
+  }
+  __syncthreads();
+  const float* E = M.w[P_EMB].p;
+  const float* g_in = M.w[P_IN_LN_G].p;
+  const float* b_in = M.w[P_IN_LN_B].p;
+  const int n4 = (d.C - kTfD) / 4;        // float4 count the roll moves
+  for (int b = blockIdx.x * kTfWarps + w; b < d.B; b += gridDim.x * kTfWarps) {
+    const long long rH = (long long)b * kTfH;
+    const int sym = lane < kTfT ? src[(long long)b * ld_src + c0 + lane] : 0;
+    float es[kTfT];
+#pragma unroll
+    for (int t = 0; t < kTfT; ++t) es[t] = E[__shfl_sync(0xffffffffu, sym, t) * kTfD + lane];
+    float* crow = M.a.cache + (long long)b * d.C;
+    // input LayerNorm over the flattened window (ops.py:94-101)
+    float s = 0.f;
+#pragma unroll
+    for (int t = 0; t < kTfT; ++t) s += es[t];
+    const float mu = warp_sum(s) / (float)kTfH;
+    float q = 0.f;
+#pragma unroll
+    for (int t = 0; t < kTfT; ++t) {
+      const float c = es[t] - mu;
+      q += c * c;
+    }
+    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(warp_sum(q) / (float)kTfH + kLnEps));
+    float x15 = 0.f;
+#pragma unroll
+    for (int t = 0; t < kTfT; ++t) {
+      const int j = t * kTfD + lane;
+      const float xh = (es[t] - mu) * inv;
+      const float xv = xh * g_in[j] + b_in[j];
+      M.a.x_hat[rH + j] = xh;
+      M.a.x[rH + j] = xv;
+      M.a.x_tc[rH + j] = tf32_rne(xv);
+      if (t == kTfT - 1) x15 = xv;
+    }
+    if (lane == 0) M.a.x_inv[b] = inv;
+    if (vf.global) {
+      // roll the cache in place (new[j] = old[j + D]) eight float4 per lane
+      // at a time: every group's loads precede its stores, and a store only
+      // overwrites data a load of the same or an earlier group has read
+      for (int base = 0; base < n4; base += 8 * 32) {
+        float4 r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int qq = base + u * 32 + lane;
+          if (qq < n4) r[u] = *(const float4*)(crow + kTfD + 4 * qq);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int qq = base + u * 32 + lane;
+          if (qq < n4) *(float4*)(crow + 4 * qq) = r[u];
+        }
+      }
+      // GeGLU block of the newest symbol: output o = lane, x_t[i] from lane i
+      float g = 0.f, v = 0.f;
+#pragma unroll
+      for (int i = 0; i < kTfD; ++i) {
+        const float xi = __shfl_sync(0xffffffffu, x15, i);
+        g += xi * wg[i * kTfD + lane];
+        v += xi * wv[i * kTfD + lane];
+      }
+      M.a.gpre[(long long)b * kTfD + lane] = g;
+      M.a.vpre[(long long)b * kTfD + lane] = v;
+      crow[d.C - kTfD + lane] = tf32_rne(gelu_f(g) * v);
+    }
+    if (vf.local) {
+      // per-symbol LayerNorm over D (ops.py:94-101 on (B,T,D))
+      const float* lg = M.w[P_LOC_LN_G].p;
+      const float* lb = M.w[P_LOC_LN_B].p;
+      const float gl = lg[lane], bl = lb[lane];
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) {
+        const float m = warp_sum(es[t]) / (float)kTfD;
+        const float c = es[t] - m;
+        const float tinv = __fdiv_rn(1.0f, __fsqrt_rn(warp_sum(c * c) / (float)kTfD + kLnEps));
+        if (lane == 0) M.a.loc_inv[(long long)b * kTfT + t] = tinv;
+        const float lh = c * tinv;
+        const float lv = lh * gl + bl;
+        M.a.loc_hat[rH + t * kTfD + lane] = lh;
+        M.a.loc[rH + t * kTfD + lane] = lv;
+        locw[t * kTfD + lane] = lv;
+      }
+      __syncwarp();
+      // same-padded conv (ops.py:57-72), output channel co = lane: input
+      // symbol s feeds outputs s + 1 (tap 0), s (tap 1) and s - 1 (tap 2)
+      float acc[kTfT];
+      const float cb = M.w[P_CONV_B].p[lane];
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) acc[t] = 0.f;
+      const float4* l4 = (const float4*)locw;
+#pragma unroll 1
+      for (int c4 = 0; c4 < kTfD / 4; ++c4) {
+        float k[kTfK][4];
+#pragma unroll
+        for (int tap = 0; tap < kTfK; ++tap)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) k[tap][c] = ck[(tap * kTfD + 4 * c4 + c) * kTfD + lane];
+#pragma unroll
+        for (int sidx = 0; sidx < kTfT; ++sidx) {
+          const float4 l = l4[sidx * (kTfD / 4) + c4];
+          const float lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (sidx + 1 < kTfT) acc[sidx + 1] += lv[c] * k[0][c];
+            acc[sidx] += lv[c] * k[1][c];
+            if (sidx >= 1) acc[sidx - 1] += lv[c] * k[2][c];
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) {
+        const float a = cb + acc[t];
+        M.a.conv_pre[rH + t * kTfD + lane] = a;
+        M.a.h_l[rH + t * kTfD + lane] = gelu_f(a);
+      }
+      __syncwarp();   // locw is rewritten by the warp's next row
+    }
+  }
+}
+
+bool launch_trunk_fwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                        cudaStream_t s) {
+  const Dims& d = M.d;
+  if (d.D != kTfD || d.T != kTfT || d.K != kTfK || M.ring_on || d.C % 4) return false;
+  const size_t smem = sizeof(float) * kTfSmemFloats;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_trunk_fwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  (void)attr;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(cdiv(d.B, kTfWarps), 2 * sms);
+  launch_pdl(k_trunk_fwd_w, dim3(grid), dim3(32 * kTfWarps), smem, s, M, src, ld_src, use_col);
+  return true;
+}
+
 // dispatch: returns false when the geometry needs the CTA-per-row kernels
 
 #define ROW_LAUNCH(kern)                                                              \

@@ -95,26 +95,30 @@ import numpy as np
 sys.path.insert(0, {root!r})
 from paper_2604_07239_b200 import ModelConfig, corpus
 from paper_2604_07239_b200.model import Predictor
-cfg = ModelConfig(ctx_len=8, embed_dim=16, cache_dim=256, mix_dim=32, expand_dim=256, batch=64,
-                  workers=1, seed=4)
-mat = np.frombuffer(corpus.make_text(64 * 20, 3), np.uint8).reshape(64, 20)
+cfg = ModelConfig(batch=64, workers=1, seed=4, **{dims!r})
+T = cfg.ctx_len
+mat = np.frombuffer(corpus.make_text(64 * (T + 6), 3), np.uint8).reshape(64, T + 6)
 out = {{}}
 for v in {variants!r}:
     m = Predictor(cfg, v)
     rows = []
-    for i in range(8, 14):
-        p = m.predict(mat[:, i - 8:i])
+    for i in range(T, T + 6):
+        p = m.predict(mat[:, i - T:i])
         rows.append([p[:4].tolist(), m.train_step(mat[:, i])])
     out[v] = rows
 print(json.dumps(out))
 """
 
 
-def test_warp_and_cta_row_kernels_agree_on_every_variant():
+@pytest.mark.parametrize("dims", [
+    dict(ctx_len=8, embed_dim=16, cache_dim=256, mix_dim=32, expand_dim=256),
+    # H = 512 at D = 32, T = 16, K = 3: also the warp-per-row trunk forward
+    dict(ctx_len=16, embed_dim=32, cache_dim=512, mix_dim=32, expand_dim=512)])
+def test_warp_and_cta_row_kernels_agree_on_every_variant(dims):
     """The warp-per-row kernels (row_warp.cu, used from B = 2048) and the
     CTA-per-row kernels compute the same thing for every variant's flags:
-    the experiments build runs both at H = 128 (FADE_ROW_WARP = 63 / 0) and
-    the trajectories agree to fp32 reduction-order noise."""
+    the experiments build runs both (FADE_ROW_WARP = 127 / 0) and the
+    trajectories agree to fp32 reduction-order noise."""
     import json
     import os
     import subprocess
@@ -123,15 +127,15 @@ def test_warp_and_cta_row_kernels_agree_on_every_variant():
     lib = os.path.join(ROOT, "build", "exp", "libfade_b200.so")
     if not os.path.exists(lib):
         pytest.skip("experiments build (make experiments) not present")
-    code = ROW_PROBE.format(root=ROOT, variants=VARIANTS)
+    code = ROW_PROBE.format(root=ROOT, variants=VARIANTS, dims=dims)
     res = {}
-    for mask in ("0", "63"):
+    for mask in ("0", "127"):
         env = dict(os.environ, FADE_LIB_PATH=lib, FADE_ROW_WARP=mask)
         out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                              timeout=600)
         assert out.returncode == 0, out.stderr[-3000:]
         res[mask] = json.loads(out.stdout.strip().splitlines()[-1])
     for v in VARIANTS:
-        for (p0, l0), (p1, l1) in zip(res["0"][v], res["63"][v]):
+        for (p0, l0), (p1, l1) in zip(res["0"][v], res["127"][v]):
             assert np.abs(np.array(p0) - np.array(p1)).max() < 1e-4, v
             assert abs(l0 - l1) < 1e-4, v

@@ -606,6 +606,7 @@ static int allocate(fade_model* m) {
   F(&a.da12, B * 2 * Ep); F(&a.ws_dz2, (long long)M.splits_dz2 * B * H); F(&a.dinner, B * H);
   F(&a.dcpre, B * H); F(&a.dzd, B * X);
   F(&a.drpre, B * H); F(&a.dupre, B * H); F(&a.dh_l, B * H); F(&a.dx_part, B * H);
+  F(&a.tb_dx, B * H); F(&a.tb_dls, B * H);
   F(&a.rowred, B * m->sl.rowred);
   {
     int dev = 0, sms = 148;

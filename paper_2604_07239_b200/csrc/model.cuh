@@ -100,6 +100,7 @@ struct Acts {        // saved activations and gradient scratch, all [B][ld]
   // backward
   float *dlogits, *dhc, *dnpre, *da12, *ws_dz2, *dinner, *dcpre;
   float *dzd, *drpre, *dupre, *dh_l, *dx_part;
+  float *tb_dx, *tb_dls;        // [B][H] trunk backward at large B: dx and dloc rows
   float *rowred;                // [B][rowred]
   float *trunk_part;            // [trunk_grid][trunk1 - trunk0] per-CTA sums of trunk_bwd
   long long* emb_acc;           // [256][D] embedding gradient, fixed point (emb_to_fixed)
@@ -152,6 +153,8 @@ bool launch_out_bwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_coarse_bwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_mix_bwd_w(const ModelPtrs& M, cudaStream_t s);
 bool launch_trunk_fwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                        cudaStream_t s);
+bool launch_trunk_bwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                         cudaStream_t s);
 bool row_warp_enabled(int B, int which);   // which: 0 mix_fwd .. 5 mix_bwd
 

@@ -1504,6 +1504,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_bwd(ModelPtrs M, con
 void launch_trunk_bwd(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                       cudaStream_t s) {
   const Dims& d = M.d;
+  if (row_warp_enabled(d.B, 7) && launch_trunk_bwd_w(M, src, ld_src, use_col, s)) return;
   const bool multi = d.B > M.trunk_grid;
   const size_t smem =
       sizeof(float) * (6 * d.H + d.K * d.D * (d.D + 1) + 3 * d.D + 32 + ((d.T + 3) & ~3)) +

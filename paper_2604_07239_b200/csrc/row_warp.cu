@@ -614,6 +614,333 @@ bool launch_trunk_fwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// trunk + local stream backward at large B, in two launches (model.py:118-137
+// backward; the compiled geometry D = 32, T = 16, K = 3 only):
+//  * k_trunk_bwd_w, warp per row: the input-gradient chain (dx_t through
+//    W_gate / W_val, the input LayerNorm backward, the conv input gradient,
+//    the per-symbol LayerNorm backward, the embedding-gradient atomics).  It
+//    leaves the row's pre-LayerNorm gradient dx and the conv input gradient
+//    dloc in two [B][H] scratch rows for
+//  * k_trunk_grads: the small-parameter gradients (in_g, in_b, loc_g, loc_b,
+//    conv_b, conv_k, w_gate, w_val) as per-CTA sums over rows b = cta, cta +
+//    grid, ... into trunk_part -- the layout k_small_adam reduces -- with
+//    per-row sums in the order of k_trunk_bwd's multi-row path.
+// Against the one-CTA-per-row k_trunk_bwd (eight warps through a chain of
+// barrier-separated phases per row) the rows of a warp need no barrier.
+__device__ __forceinline__ float split_at(const SplitBuf& k, long long plane, long long idx) {
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int s = 0; s < k.S; ++s) a[s & 3] += k.ws[s * plane + idx];
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
+constexpr int kTbWarps = 8;
+// smem: W_gate^T, W_val^T [o][i], taps transposed [tap][co][ci], per-warp dconv
+// window, then the CTA's embedding-gradient table [256][D] (int64 fixed point)
+// and its touched-symbol flags
+constexpr int kTbSmemFloats = 2 * kTfD * kTfD + kTfK * kTfD * kTfD + kTbWarps * kTfH;
+constexpr size_t kTbSmemBytes = sizeof(float) * kTbSmemFloats + sizeof(long long) * 256 * kTfD +
+                                sizeof(int) * 256;
+
+__global__ void __launch_bounds__(32 * kTbWarps, 2) k_trunk_bwd_w(ModelPtrs M, const uint8_t* src,
+                                                                 long long ld_src, int use_col) {
+  pdl_enter();
+  extern __shared__ float4 tb_sm4[];
+  float* wgt = (float*)tb_sm4;               // [o][i] = W_gate[i][o]
+  float* wvt = wgt + kTfD * kTfD;            // [o][i] = W_val[i][o]
+  float* ckt = wvt + kTfD * kTfD;            // [tap][co][ci] = conv_k[tap][ci][co]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  float* dcw = ckt + kTfK * kTfD * kTfD + w * kTfH;   // this warp's dconv window [t][co]
+  // embedding-gradient rows of this CTA's rows, summed in shared memory first:
+  // the global atomics then see one add per (CTA, symbol, channel) instead of
+  // one per (row, position) -- frequent symbols no longer serialise on L2
+  unsigned long long* eacc =
+      (unsigned long long*)(ckt + kTfK * kTfD * kTfD + kTbWarps * kTfH);
+  int* touched = (int*)(eacc + 256 * kTfD);
+  for (int j = tid; j < 256 * kTfD; j += blockDim.x) eacc[j] = 0ull;
+  for (int j = tid; j < 256; j += blockDim.x) touched[j] = 0;
+  const VFlags vf = vflags(M.variant);
+  const Dims& d = M.d;
+  const long long c0 = use_col ? M.st->col - kTfT : 0;
+  for (int j = tid; j < kTfD * kTfD; j += blockDim.x) {
+    const int i = j / kTfD, o = j % kTfD;
+    wgt[o * kTfD + i] = M.w[P_W_GATE].p[j];
+    wvt[o * kTfD + i] = M.w[P_W_VAL].p[j];
+  }
+  for (int j = tid; j < kTfK * kTfD * kTfD; j += blockDim.x) {
+    const int tap = j / (kTfD * kTfD), ci = (j / kTfD) % kTfD, co = j % kTfD;
+    ckt[(tap * kTfD + co) * kTfD + ci] = M.w[P_CONV_K].p[j];
+  }
+  __syncthreads();
+  const float* gin = M.w[P_IN_LN_G].p;
+  const float gl = M.w[P_LOC_LN_G].p[lane];
+  const long long planeH = (long long)d.B * kTfH, planeD = (long long)d.B * kTfD;
+  for (int b = blockIdx.x * kTbWarps + w; b < d.B; b += gridDim.x * kTbWarps) {
+    const long long rH = (long long)b * kTfH;
+    const int sym = lane < kTfT ? src[(long long)b * ld_src + c0 + lane] : 0;
+    // every load of the row first (independent, all in flight), then the sums
+    float dx[kTfT], xh[kTfT], dp[kTfT];
+#pragma unroll
+    for (int t = 0; t < kTfT; ++t) {
+      const long long j = rH + t * kTfD + lane;
+      xh[t] = M.a.x_hat[j];
+      dp[t] = vf.global ? M.a.dx_part[j] : 0.f;
+      dx[t] = (vf.router && M.sk[S_DXR].S == 1) ? M.sk[S_DXR].ws[j] : 0.f;
+    }
+    // dx_t through the GeGLU block (lane = input i; dg / dv of output o from lane o)
+    float dxt = 0.f;
+    if (vf.global) {
+      const float gp = M.a.gpre[(long long)b * kTfD + lane];
+      const float vp = M.a.vpre[(long long)b * kTfD + lane];
+      const float db = M.sk[S_DBLOCK].S == 1 ? M.sk[S_DBLOCK].ws[(long long)b * kTfD + lane]
+                                              : split_at(M.sk[S_DBLOCK], planeD, (long long)b * kTfD + lane);
+      const float dg = db * vp * gelu_grad_f(gp), dv = db * gelu_f(gp);
+      float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+      for (int o = 0; o < kTfD; ++o) {
+        a1 += __shfl_sync(0xffffffffu, dg, o) * wgt[o * kTfD + lane];
+        a2 += __shfl_sync(0xffffffffu, dv, o) * wvt[o * kTfD + lane];
+      }
+      dxt = a1 + a2;
+    }
+    // dx (router + global skip + dx_t) and the input LayerNorm backward
+    if (vf.router && M.sk[S_DXR].S != 1)
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) dx[t] = split_at(M.sk[S_DXR], planeH, rH + t * kTfD + lane);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int t = 0; t < kTfT; ++t) {
+      const long long j = rH + t * kTfD + lane;
+      float v = dx[t];
+      if (vf.global) v = vf.router ? v + dp[t] : dp[t];
+      if (t == kTfT - 1) v += dxt;
+      dx[t] = v;
+      xh[t] = M.a.x_hat[j];
+      M.a.tb_dx[j] = v;
+      const float gg = v * gin[t * kTfD + lane];
+      s1 += gg;
+      s2 += gg * xh[t];
+    }
+    const float m1 = warp_sum(s1) / (float)kTfH, m2 = warp_sum(s2) / (float)kTfH;
+    const float xinv = M.a.x_inv[b];
+#pragma unroll
+    for (int t = 0; t < kTfT; ++t) dx[t] = (dx[t] * gin[t * kTfD + lane] - m1 - xh[t] * m2) * xinv;
+    if (vf.local) {
+      // dconv (lane = co) staged for the broadcast reads of the input gradient
+      float lh[kTfT], li[kTfT];
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) {
+        const long long j = rH + t * kTfD + lane;
+        lh[t] = M.a.loc_hat[j];
+        li[t] = M.a.loc_inv[(long long)b * kTfT + t];
+        dcw[t * kTfD + lane] = M.a.dh_l[j] * gelu_grad_f(M.a.conv_pre[j]);
+      }
+      __syncwarp();
+      // conv input gradient, lane = ci: output t of tap `tap` read input
+      // symbol s = t + tap - 1 (ops.py:74-88)
+      float dl[kTfT];
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) dl[t] = 0.f;
+      const float4* g4 = (const float4*)dcw;
+#pragma unroll 1
+      for (int c4 = 0; c4 < kTfD / 4; ++c4) {
+        float k[kTfK][4];
+#pragma unroll
+        for (int tap = 0; tap < kTfK; ++tap)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) k[tap][c] = ckt[(tap * kTfD + 4 * c4 + c) * kTfD + lane];
+#pragma unroll
+        for (int t = 0; t < kTfT; ++t) {
+          const float4 g = g4[t * (kTfD / 4) + c4];
+          const float gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (t >= 1) dl[t - 1] += gv[c] * k[0][c];
+            dl[t] += gv[c] * k[1][c];
+            if (t + 1 < kTfT) dl[t + 1] += gv[c] * k[2][c];
+          }
+        }
+      }
+      // per-symbol LayerNorm backward over D, lane = channel e
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) {
+        const long long j = rH + t * kTfD + lane;
+        M.a.tb_dls[j] = dl[t];
+        const float gg = dl[t] * gl;
+        const float q1 = warp_sum(gg) / (float)kTfD, q2 = warp_sum(gg * lh[t]) / (float)kTfD;
+        dx[t] += (gg - q1 - lh[t] * q2) * li[t];
+      }
+      __syncwarp();   // dcw is rewritten by the warp's next row
+    }
+    // embedding gradient (ops.py:234-243 scatter-add), fixed point: the
+    // integer sums do not depend on the order the rows arrive in
+#pragma unroll
+    for (int t = 0; t < kTfT; ++t) {
+      const int sy = __shfl_sync(0xffffffffu, sym, t);
+      atomicAdd(&eacc[sy * kTfD + lane], (unsigned long long)emb_to_fixed(dx[t]));
+      if (lane == 0) touched[sy] = 1;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < 256 * kTfD; j += blockDim.x)
+    if (touched[j / kTfD] && !(M.dbg & 1))
+      atomicAdd((unsigned long long*)&M.a.emb_acc[j], eacc[j]);
+}
+
+// Small-parameter gradients of the trunk from the rows' saved activations and
+// k_trunk_bwd_w's dx / dloc rows: per-CTA sums (rows b = cta, cta + grid, ...)
+// into trunk_part[cta] -- one owner thread per column.
+constexpr int kTgThreads = 256;
+__global__ void __launch_bounds__(kTgThreads, 4) k_trunk_grads(ModelPtrs M) {
+  pdl_enter();
+  __shared__ __align__(16) float loc[kTfH], dcv[kTfH], dxr[kTfH], xhr[kTfH], dls[kTfH], lhr[kTfH];
+  __shared__ float xt[kTfD], dg[kTfD], dv[kTfD];
+  const int tid = threadIdx.x;
+  const VFlags vf = vflags(M.variant);
+  const Dims& d = M.d;
+  const long long planeD = (long long)d.B * kTfD;
+  // conv_k: co = tid % 32, ci = 4 * (tid / 32) + c, all three taps
+  const int co = tid & 31, ci0 = 4 * (tid >> 5);
+  float ak[kTfK][4] = {}, agv[8] = {}, ain[4] = {};
+  float acb = 0.f, alg = 0.f, alb = 0.f;
+  // the next row's loads are issued (into registers) before this row's sums:
+  // one row's L2 round trip hides behind the previous row's arithmetic
+  float r_dx[2], r_xh[2], r_loc[2], r_dh[2], r_cp[2], r_dls[2], r_lh[2];
+  float r_gp = 0.f, r_vp = 0.f, r_db = 0.f, r_xt = 0.f;
+  auto load = [&](int b) {
+    const long long rH = (long long)b * kTfH;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const long long j = rH + tid + kTgThreads * k;
+      r_dx[k] = M.a.tb_dx[j];
+      r_xh[k] = M.a.x_hat[j];
+      if (vf.local) {
+        r_loc[k] = M.a.loc[j];
+        r_dh[k] = M.a.dh_l[j];
+        r_cp[k] = M.a.conv_pre[j];
+        r_dls[k] = M.a.tb_dls[j];
+        r_lh[k] = M.a.loc_hat[j];
+      }
+    }
+    if (vf.global && tid < kTfD) {
+      r_gp = M.a.gpre[(long long)b * kTfD + tid];
+      r_vp = M.a.vpre[(long long)b * kTfD + tid];
+      r_db = split_at(M.sk[S_DBLOCK], planeD, (long long)b * kTfD + tid);
+      r_xt = M.a.x[rH + kTfH - kTfD + tid];
+    }
+  };
+  if ((int)blockIdx.x < d.B) load(blockIdx.x);
+  for (int b = blockIdx.x; b < d.B; b += gridDim.x) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int j = tid + kTgThreads * k;
+      dxr[j] = r_dx[k];
+      xhr[j] = r_xh[k];
+      if (vf.local) {
+        loc[j] = r_loc[k];
+        dcv[j] = r_dh[k] * gelu_grad_f(r_cp[k]);
+        dls[j] = r_dls[k];
+        lhr[j] = r_lh[k];
+      }
+    }
+    if (vf.global && tid < kTfD) {
+      dg[tid] = r_db * r_vp * gelu_grad_f(r_gp);
+      dv[tid] = r_db * gelu_f(r_gp);
+      xt[tid] = r_xt;
+    }
+    __syncthreads();
+    if (b + (int)gridDim.x < d.B) load(b + gridDim.x);
+    if (vf.global) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int q = tid + kTgThreads * k, i = q / kTfD, o = q % kTfD;
+        agv[k] += xt[i] * dg[o];
+        agv[4 + k] += xt[i] * dv[o];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int j = tid + kTgThreads * k;
+      ain[k] += dxr[j] * xhr[j];
+      ain[2 + k] += dxr[j];
+    }
+    if (vf.local) {
+      // per row: sum over t ascending of loc[t + tap - 1][ci] * dcv[t][co]
+      float r[kTfK][4] = {};
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) {
+        const float g = dcv[t * kTfD + co];
+#pragma unroll
+        for (int tap = 0; tap < kTfK; ++tap) {
+          const int sidx = t + tap - kTfK / 2;
+          if (sidx < 0 || sidx >= kTfT) continue;
+          const float4 l = *(const float4*)(loc + sidx * kTfD + ci0);
+          r[tap][0] += l.x * g;
+          r[tap][1] += l.y * g;
+          r[tap][2] += l.z * g;
+          r[tap][3] += l.w * g;
+        }
+      }
+#pragma unroll
+      for (int tap = 0; tap < kTfK; ++tap)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ak[tap][c] += r[tap][c];
+      if (tid < kTfD) {
+        float cbs = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int t = 0; t < kTfT; ++t) {
+          cbs += dcv[t * kTfD + tid];
+          s1 += dls[t * kTfD + tid] * lhr[t * kTfD + tid];
+          s2 += dls[t * kTfD + tid];
+        }
+        acb += cbs;
+        alg += s1;
+        alb += s2;
+      }
+    }
+    __syncthreads();   // the next row overwrites the staged rows
+  }
+  const SmallLayout& L = M.sl;
+  float* part = M.a.trunk_part + (long long)blockIdx.x * (L.trunk1 - L.trunk0) - L.trunk0;
+#pragma unroll
+  for (int tap = 0; tap < kTfK; ++tap)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) part[L.conv_k + tap * kTfD * kTfD + (ci0 + c) * kTfD + co] = ak[tap][c];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    part[L.w_gate + tid + kTgThreads * k] = agv[k];
+    part[L.w_val + tid + kTgThreads * k] = agv[4 + k];
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    part[L.in_g + tid + kTgThreads * k] = ain[k];
+    part[L.in_b + tid + kTgThreads * k] = ain[2 + k];
+  }
+  if (tid < kTfD) {
+    part[L.conv_b + tid] = acb;
+    part[L.loc_g + tid] = alg;
+    part[L.loc_b + tid] = alb;
+  }
+}
+
+bool launch_trunk_bwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
+                        cudaStream_t s) {
+  const Dims& d = M.d;
+  if (d.D != kTfD || d.T != kTfT || d.K != kTfK || !M.a.tb_dx) return false;
+  const size_t smem = kTbSmemBytes;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_trunk_bwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  (void)attr;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(cdiv(d.B, kTbWarps), 2 * sms);
+  launch_pdl(k_trunk_bwd_w, dim3(grid), dim3(32 * kTbWarps), smem, s, M, src, ld_src, use_col);
+  launch_pdl(k_trunk_grads, dim3(M.trunk_grid), dim3(kTgThreads), 0, s, M);
+  return true;
+}
+
 // dispatch: returns false when the geometry needs the CTA-per-row kernels
 
 #define ROW_LAUNCH(kern)                                                              \

@@ -117,7 +117,7 @@ print(json.dumps(out))
 def test_warp_and_cta_row_kernels_agree_on_every_variant(dims):
     """The warp-per-row kernels (row_warp.cu, used from B = 2048) and the
     CTA-per-row kernels compute the same thing for every variant's flags:
-    the experiments build runs both (FADE_ROW_WARP = 127 / 0) and the
+    the experiments build runs both (FADE_ROW_WARP = 255 / 0) and the
     trajectories agree to fp32 reduction-order noise."""
     import json
     import os
@@ -129,13 +129,13 @@ def test_warp_and_cta_row_kernels_agree_on_every_variant(dims):
         pytest.skip("experiments build (make experiments) not present")
     code = ROW_PROBE.format(root=ROOT, variants=VARIANTS, dims=dims)
     res = {}
-    for mask in ("0", "127"):
+    for mask in ("0", "255"):
         env = dict(os.environ, FADE_LIB_PATH=lib, FADE_ROW_WARP=mask)
         out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                              timeout=600)
         assert out.returncode == 0, out.stderr[-3000:]
         res[mask] = json.loads(out.stdout.strip().splitlines()[-1])
     for v in VARIANTS:
-        for (p0, l0), (p1, l1) in zip(res["0"][v], res["127"][v]):
+        for (p0, l0), (p1, l1) in zip(res["0"][v], res["255"][v]):
             assert np.abs(np.array(p0) - np.array(p1)).max() < 1e-4, v
             assert abs(l0 - l1) < 1e-4, v

@@ -101,6 +101,7 @@ struct fade_model {
   cudaStream_t s_main = nullptr, s_side = nullptr, s_coder = nullptr;
   cudaStream_t s_side2 = nullptr;   // second weight-update stream (side2_mask)
   cudaEvent_t ev_side2_done = nullptr;
+  cudaEvent_t ev_tg[2] = {};        // large-B trunk weight gradients on s_side2: fork / join
   cudaEvent_t ev[8] = {};
   cudaEvent_t ev_cum[2] = {}, ev_enc[2] = {}, ev_side_done = nullptr, ev_coder_join = nullptr;
   cudaEvent_t ev_wu[2] = {};    // W_U update forked off the model stream (experiments)
@@ -817,8 +818,19 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   TRY(sides());
   TRY(run_gemm(m, G_DXR_DBLOCK, s));
   TRY(sides());
+  // large B: the conv / GeGLU weight gradients of the trunk need only the
+  // dx_r / dblock GEMM's outputs -- on the second side stream beside the
+  // trunk input-gradient chain, joined before small_adam
+  const bool tsplit = trunk_bwd_split(M);
+  if (tsplit) {
+    CK(cudaEventRecord(m->ev_tg[0], s));
+    CK(cudaStreamWaitEvent(m->s_side2, m->ev_tg[0], 0));
+    launch_trunk_grads_conv(M, m->s_side2);
+    CK(cudaEventRecord(m->ev_tg[1], m->s_side2));
+  }
   launch_trunk_bwd(M, io.src, io.ld_src, io.use_col, s);
   TRY(sides());
+  if (tsplit) CK(cudaStreamWaitEvent(s, m->ev_tg[1], 0));
   launch_small_adam(M, grad_only, losses, io.alpha_tape, advance, s);
   CK(cudaEventRecord(m->ev_side_done, side));
   CK(cudaStreamWaitEvent(s, m->ev_side_done, 0));
@@ -1010,6 +1022,7 @@ int fade_model_create(const fade_config_t* cfg, int device, fade_model_t** out) 
   CK(cudaStreamCreateWithPriority(&m->s_side, cudaStreamNonBlocking, prio_lo));
   CK(cudaStreamCreateWithPriority(&m->s_side2, cudaStreamNonBlocking, prio_lo));
   CK(cudaEventCreateWithFlags(&m->ev_side2_done, cudaEventDisableTiming));
+  for (auto& e : m->ev_tg) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaStreamCreateWithPriority(&m->s_coder, cudaStreamNonBlocking, prio_hi));
   for (auto& e : m->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
@@ -1055,6 +1068,7 @@ int fade_model_destroy(fade_model_t* m) {
   }
   cudaEventDestroy(m->ev_side_done);
   cudaEventDestroy(m->ev_side2_done);
+  for (auto& e : m->ev_tg) cudaEventDestroy(e);
   cudaEventDestroy(m->ev_coder_join);
   for (auto& e : m->ev_wu) cudaEventDestroy(e);
   cudaStreamDestroy(m->s_main);

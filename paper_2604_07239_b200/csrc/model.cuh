@@ -156,6 +156,12 @@ bool launch_trunk_fwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src
                         cudaStream_t s);
 bool launch_trunk_bwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                         cudaStream_t s);
+// large-B trunk backward (row_warp.cu): true when launch_trunk_bwd runs the
+// warp-per-row input-gradient kernel + the in/loc LayerNorm gradient kernel,
+// and the caller runs launch_trunk_grads_conv (conv / GeGLU weight gradients,
+// ready after the dx_r GEMM) on a second stream before small_adam
+bool trunk_bwd_split(const ModelPtrs& M);
+void launch_trunk_grads_conv(const ModelPtrs& M, cudaStream_t s);
 bool row_warp_enabled(int B, int which);   // which: 0 mix_fwd .. 5 mix_bwd
 
 // row kernels (model_kernels.cu)

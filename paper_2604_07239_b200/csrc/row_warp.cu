@@ -791,13 +791,20 @@ __global__ void __launch_bounds__(32 * kTbWarps, 2) k_trunk_bwd_w(ModelPtrs M, c
 // Small-parameter gradients of the trunk from the rows' saved activations and
 // k_trunk_bwd_w's dx / dloc rows: per-CTA sums (rows b = cta, cta + grid, ...)
 // into trunk_part[cta] -- one owner thread per column.
+// PART 1: conv_k, conv_b, w_gate, w_val (inputs ready after the dx_r / dblock
+// GEMM: runs on a second stream beside k_trunk_bwd_w); PART 2: in_g, in_b,
+// loc_g, loc_b (needs k_trunk_bwd_w's dx / dloc rows)
 constexpr int kTgThreads = 256;
+template <int PART>
 __global__ void __launch_bounds__(kTgThreads, 4) k_trunk_grads(ModelPtrs M) {
   pdl_enter();
   __shared__ __align__(16) float loc[kTfH], dcv[kTfH], dxr[kTfH], xhr[kTfH], dls[kTfH], lhr[kTfH];
   __shared__ float xt[kTfD], dg[kTfD], dv[kTfD];
   const int tid = threadIdx.x;
-  const VFlags vf = vflags(M.variant);
+  const VFlags vf0 = vflags(M.variant);
+  // the flags of what this part computes
+  const bool loc_on = vf0.local, glob_on = PART == 1 && vf0.global;
+  const bool conv_on = PART == 1 && loc_on, lnl_on = PART == 2 && loc_on;
   const Dims& d = M.d;
   const long long planeD = (long long)d.B * kTfD;
   // conv_k: co = tid % 32, ci = 4 * (tid / 32) + c, all three taps
@@ -813,17 +820,21 @@ __global__ void __launch_bounds__(kTgThreads, 4) k_trunk_grads(ModelPtrs M) {
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const long long j = rH + tid + kTgThreads * k;
-      r_dx[k] = M.a.tb_dx[j];
-      r_xh[k] = M.a.x_hat[j];
-      if (vf.local) {
+      if (PART == 2) {
+        r_dx[k] = M.a.tb_dx[j];
+        r_xh[k] = M.a.x_hat[j];
+      }
+      if (conv_on) {
         r_loc[k] = M.a.loc[j];
         r_dh[k] = M.a.dh_l[j];
         r_cp[k] = M.a.conv_pre[j];
+      }
+      if (lnl_on) {
         r_dls[k] = M.a.tb_dls[j];
         r_lh[k] = M.a.loc_hat[j];
       }
     }
-    if (vf.global && tid < kTfD) {
+    if (glob_on && tid < kTfD) {
       r_gp = M.a.gpre[(long long)b * kTfD + tid];
       r_vp = M.a.vpre[(long long)b * kTfD + tid];
       r_db = split_at(M.sk[S_DBLOCK], planeD, (long long)b * kTfD + tid);
@@ -835,23 +846,27 @@ __global__ void __launch_bounds__(kTgThreads, 4) k_trunk_grads(ModelPtrs M) {
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int j = tid + kTgThreads * k;
-      dxr[j] = r_dx[k];
-      xhr[j] = r_xh[k];
-      if (vf.local) {
+      if (PART == 2) {
+        dxr[j] = r_dx[k];
+        xhr[j] = r_xh[k];
+      }
+      if (conv_on) {
         loc[j] = r_loc[k];
         dcv[j] = r_dh[k] * gelu_grad_f(r_cp[k]);
+      }
+      if (lnl_on) {
         dls[j] = r_dls[k];
         lhr[j] = r_lh[k];
       }
     }
-    if (vf.global && tid < kTfD) {
+    if (glob_on && tid < kTfD) {
       dg[tid] = r_db * r_vp * gelu_grad_f(r_gp);
       dv[tid] = r_db * gelu_f(r_gp);
       xt[tid] = r_xt;
     }
     __syncthreads();
     if (b + (int)gridDim.x < d.B) load(b + gridDim.x);
-    if (vf.global) {
+    if (glob_on) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int q = tid + kTgThreads * k, i = q / kTfD, o = q % kTfD;
@@ -859,13 +874,14 @@ __global__ void __launch_bounds__(kTgThreads, 4) k_trunk_grads(ModelPtrs M) {
         agv[4 + k] += xt[i] * dv[o];
       }
     }
+    if (PART == 2)
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int j = tid + kTgThreads * k;
-      ain[k] += dxr[j] * xhr[j];
-      ain[2 + k] += dxr[j];
-    }
-    if (vf.local) {
+      for (int k = 0; k < 2; ++k) {
+        const int j = tid + kTgThreads * k;
+        ain[k] += dxr[j] * xhr[j];
+        ain[2 + k] += dxr[j];
+      }
+    if (conv_on) {
       // per row: sum over t ascending of loc[t + tap - 1][ci] * dcv[t][co]
       float r[kTfK][4] = {};
 #pragma unroll
@@ -887,47 +903,54 @@ __global__ void __launch_bounds__(kTgThreads, 4) k_trunk_grads(ModelPtrs M) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) ak[tap][c] += r[tap][c];
       if (tid < kTfD) {
-        float cbs = 0.f, s1 = 0.f, s2 = 0.f;
+        float cbs = 0.f;
 #pragma unroll
-        for (int t = 0; t < kTfT; ++t) {
-          cbs += dcv[t * kTfD + tid];
-          s1 += dls[t * kTfD + tid] * lhr[t * kTfD + tid];
-          s2 += dls[t * kTfD + tid];
-        }
+        for (int t = 0; t < kTfT; ++t) cbs += dcv[t * kTfD + tid];
         acb += cbs;
-        alg += s1;
-        alb += s2;
       }
+    }
+    if (lnl_on && tid < kTfD) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int t = 0; t < kTfT; ++t) {
+        s1 += dls[t * kTfD + tid] * lhr[t * kTfD + tid];
+        s2 += dls[t * kTfD + tid];
+      }
+      alg += s1;
+      alb += s2;
     }
     __syncthreads();   // the next row overwrites the staged rows
   }
   const SmallLayout& L = M.sl;
   float* part = M.a.trunk_part + (long long)blockIdx.x * (L.trunk1 - L.trunk0) - L.trunk0;
+  if (PART == 1) {
 #pragma unroll
-  for (int tap = 0; tap < kTfK; ++tap)
+    for (int tap = 0; tap < kTfK; ++tap)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) part[L.conv_k + tap * kTfD * kTfD + (ci0 + c) * kTfD + co] = ak[tap][c];
+      for (int c = 0; c < 4; ++c) part[L.conv_k + tap * kTfD * kTfD + (ci0 + c) * kTfD + co] = ak[tap][c];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    part[L.w_gate + tid + kTgThreads * k] = agv[k];
-    part[L.w_val + tid + kTgThreads * k] = agv[4 + k];
-  }
+    for (int k = 0; k < 4; ++k) {
+      part[L.w_gate + tid + kTgThreads * k] = agv[k];
+      part[L.w_val + tid + kTgThreads * k] = agv[4 + k];
+    }
+    if (tid < kTfD) part[L.conv_b + tid] = acb;
+  } else {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    part[L.in_g + tid + kTgThreads * k] = ain[k];
-    part[L.in_b + tid + kTgThreads * k] = ain[2 + k];
-  }
-  if (tid < kTfD) {
-    part[L.conv_b + tid] = acb;
-    part[L.loc_g + tid] = alg;
-    part[L.loc_b + tid] = alb;
+    for (int k = 0; k < 2; ++k) {
+      part[L.in_g + tid + kTgThreads * k] = ain[k];
+      part[L.in_b + tid + kTgThreads * k] = ain[2 + k];
+    }
+    if (tid < kTfD) {
+      part[L.loc_g + tid] = alg;
+      part[L.loc_b + tid] = alb;
+    }
   }
 }
 
 bool launch_trunk_bwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src, int use_col,
                         cudaStream_t s) {
   const Dims& d = M.d;
-  if (d.D != kTfD || d.T != kTfT || d.K != kTfK || !M.a.tb_dx) return false;
+  if (!trunk_bwd_split(M)) return false;
   const size_t smem = kTbSmemBytes;
   static const cudaError_t attr =
       cudaFuncSetAttribute(k_trunk_bwd_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -937,8 +960,17 @@ bool launch_trunk_bwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = std::min(cdiv(d.B, kTbWarps), 2 * sms);
   launch_pdl(k_trunk_bwd_w, dim3(grid), dim3(32 * kTbWarps), smem, s, M, src, ld_src, use_col);
-  launch_pdl(k_trunk_grads, dim3(M.trunk_grid), dim3(kTgThreads), 0, s, M);
+  launch_pdl(k_trunk_grads<2>, dim3(M.trunk_grid), dim3(kTgThreads), 0, s, M);
   return true;
+}
+
+bool trunk_bwd_split(const ModelPtrs& M) {
+  const Dims& d = M.d;
+  return row_warp_enabled(d.B, 7) && d.D == kTfD && d.T == kTfT && d.K == kTfK && M.a.tb_dx;
+}
+
+void launch_trunk_grads_conv(const ModelPtrs& M, cudaStream_t s) {
+  launch_pdl(k_trunk_grads<1>, dim3(M.trunk_grid), dim3(kTgThreads), 0, s, M);
 }
 
 // dispatch: returns false when the geometry needs the CTA-per-row kernels

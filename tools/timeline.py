@@ -49,7 +49,7 @@ def main():
     ev.sort(key=lambda e: e["ts"])
     names = [e["name"] for e in ev]
     # one timestep = from a k_trunk_fwd to the next
-    starts = [i for i, nm in enumerate(names) if nm.startswith("void fade::k_trunk_fwd")]
+    starts = [i for i, nm in enumerate(names) if nm.startswith(("void fade::k_trunk_fwd", "fade::k_trunk_fwd"))]
     if len(starts) < 3:
         print("no timesteps found", len(ev))
         return

@@ -608,7 +608,8 @@ static int allocate(fade_model* m) {
   F(&a.dcpre, B * H); F(&a.dzd, B * X);
   F(&a.drpre, B * H); F(&a.dupre, B * H); F(&a.dh_l, B * H); F(&a.dx_part, B * H);
   F(&a.tb_dx, B * H); F(&a.tb_dls, B * H);
-  F(&a.rowred, B * m->sl.rowred);
+  M.rr_rows = rowred_rows((int)B, (int)H);
+  F(&a.rowred, (long long)M.rr_rows * m->sl.rowred);
   {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

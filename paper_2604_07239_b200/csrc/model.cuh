@@ -139,6 +139,9 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   // trunk_bwd grid: min(B, 4 per SM); each CTA loops over rows b = cta,
   // cta + grid, ... and writes one partial row of its small-parameter sums
   int trunk_grid;
+  // rows of the rowred matrix small_adam sums (rowred_rows): B, or B / 4 when
+  // the warp-per-row backward kernels write one combined row per CTA
+  int rr_rows;
   int dbg;   // experiments build only (FADE_DBG_TRUNK): bit 0 drops the embedding-gradient atomics
 };
 __device__ __forceinline__ unsigned long long* tape_at(const ModelPtrs& M, int slot) {
@@ -161,6 +164,7 @@ bool launch_trunk_bwd_w(const ModelPtrs& M, const uint8_t* src, long long ld_src
 // and the caller runs launch_trunk_grads_conv (conv / GeGLU weight gradients,
 // ready after the dx_r GEMM) on a second stream before small_adam
 bool trunk_bwd_split(const ModelPtrs& M);
+int rowred_rows(int B, int H);
 void launch_trunk_grads_conv(const ModelPtrs& M, cudaStream_t s);
 bool row_warp_enabled(int B, int which);   // which: 0 mix_fwd .. 5 mix_bwd
 

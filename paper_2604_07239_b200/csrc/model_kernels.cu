@@ -1564,7 +1564,7 @@ __global__ void __maxnreg__(40) k_small_adam(ModelPtrs M, int grad_only,
     const float* base = trunk ? M.a.trunk_part + (c - M.sl.trunk0)
                               : ((c < R) ? M.a.rowred + c : M.a.dlogits + (c - R));
     const long long ld = trunk ? M.sl.trunk1 - M.sl.trunk0 : ((c < R) ? R : kAlphabet);
-    const int rows = trunk ? M.trunk_grid : M.d.B;
+    const int rows = trunk ? M.trunk_grid : ((c < R) ? M.rr_rows : M.d.B);
     int b = w;
     for (; b + (kColAcc - 1) * kColWarps < rows; b += kColAcc * kColWarps) {
 #pragma unroll

@@ -274,11 +274,59 @@ __device__ __forceinline__ void row_ln_bwd_means(const RowV<NV>& dy, const RowV<
   *m2 = warp_sum(s2) / n;
 }
 
+// Per-row gradient columns of the small parameters (LayerNorm gains / biases
+// and the lam scalars) for k_small_adam.  M.rr_rows == B: one rowred row per
+// stream row.  M.rr_rows == B / kRowWarps (B >= 2048, all three backward row
+// kernels warp-per-row): the CTA's rows are summed in warp order (w = 0, 1, 2,
+// 3) through shared memory and written as ONE rowred row per CTA -- a quarter
+// of the bytes written here and read back by small_adam.
+template <int NV>
+__device__ __forceinline__ void rr_store(const ModelPtrs& M, int b, bool two, int off0,
+                                         const RowV<NV>& r0, int off1, const RowV<NV>& r1,
+                                         bool has_l, int offl, float l) {
+  constexpr int H = NV * 128, ld = 2 * H + 4;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (M.rr_rows == M.d.B) {
+    float* rr = M.a.rowred + (long long)b * M.sl.rowred;
+    if (two) {
+      st_row<NV>(rr + off0, r0);
+      st_row<NV>(rr + off1, r1);
+    }
+    if (has_l && lane == 0) rr[offl] = l;
+    return;
+  }
+  extern __shared__ float4 rr_sm4[];
+  float* sm = (float*)rr_sm4;
+  float* slot = sm + w * ld;
+  if (two) {
+    st_row<NV>(slot, r0);
+    st_row<NV>(slot + H, r1);
+  }
+  if (lane == 0) slot[2 * H] = l;
+  __syncthreads();
+  float* rr = M.a.rowred + (long long)blockIdx.x * M.sl.rowred;
+  for (int c = threadIdx.x; c <= 2 * H; c += blockDim.x) {
+    if (c < 2 * H ? !two : !has_l) continue;
+    float v = sm[c];
+#pragma unroll
+    for (int k = 1; k < kRowWarps; ++k) v += sm[k * ld + c];
+    rr[c < H ? off0 + c : (c < 2 * H ? off1 + c - H : offl)] = v;
+  }
+  __syncthreads();   // the slots are rewritten by a following rr_store
+}
+
+int rowred_rows(int B, int H) {
+  // (the CTA-per-row fallbacks -- H not a multiple of 128 -- write every row)
+  return (B % kRowWarps == 0 && H % 128 == 0 && H <= 1024 && row_warp_enabled(B, 3) &&
+          row_warp_enabled(B, 4) && row_warp_enabled(B, 5))
+             ? B / kRowWarps
+             : B;
+}
+
 // h = gelu(LN(npre)) + lam_out * h_c   (model.py:170-172 backward)
 template <int NV>
 __global__ void __launch_bounds__(32 * kRowWarps) k_out_bwd_w(ModelPtrs M) {
   ROW_PROLOGUE
-  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
   const float lam = M.w[P_LAM_OUT].p[0];
   const RowV<NV> dh = ld_split<NV>(M.sk[S_DH].ws, plane, rH, M.sk[S_DH].S);
   const RowV<NV> nrm = ld_row<NV>(M.a.nrm + rH), nh = ld_row<NV>(M.a.n_hat + rH);
@@ -297,11 +345,8 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_out_bwd_w(ModelPtrs M) {
       lsum += d * el(hc.v[k], e);
       el(dhc.v[k], e) = d * lam;
     }
-  st_row<NV>(rr + M.sl.out_g, rg);
-  st_row<NV>(rr + M.sl.out_b, dn);
   st_row<NV>(M.a.dhc + rH, dhc);
-  const float ls = warp_sum(lsum);
-  if (lane == 0) rr[M.sl.lam_out] = ls;
+  rr_store<NV>(M, b, true, M.sl.out_g, rg, M.sl.out_b, dn, true, M.sl.lam_out, warp_sum(lsum));
   float m1, m2;
   row_ln_bwd_means<NV>(dn, g, nh, (float)H, &m1, &m2);
   RowV<NV> dx;
@@ -317,21 +362,18 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_out_bwd_w(ModelPtrs M) {
 template <int NV>
 __global__ void __launch_bounds__(32 * kRowWarps) k_coarse_bwd_w(ModelPtrs M) {
   ROW_PROLOGUE
-  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
   const VFlags vf = vflags(M.variant);
-  RowV<NV> dhc;
+  RowV<NV> dhc, rg, rb;
   if (vf.fnr) {
     const RowV<NV> dz = ld_split<NV>(M.a.ws_dz2, plane, rH, M.splits_dz2);
     const RowV<NV> zh = ld_row<NV>(M.a.z2_hat + rH), g = ld_row<NV>(M.w[P_REF_LN_G].p);
     const RowV<NV> din = ld_row<NV>(M.a.dhc + rH);
     const float inv = M.a.z2_inv[b];
-    RowV<NV> rg;
 #pragma unroll
     for (int k = 0; k < NV; ++k)
 #pragma unroll
       for (int e = 0; e < 4; ++e) el(rg.v[k], e) = el(dz.v[k], e) * el(zh.v[k], e);
-    st_row<NV>(rr + M.sl.ref_g, rg);
-    st_row<NV>(rr + M.sl.ref_b, dz);
+    rb = dz;
     float m1, m2;
     row_ln_bwd_means<NV>(dz, g, zh, (float)H, &m1, &m2);
 #pragma unroll
@@ -360,17 +402,15 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_coarse_bwd_w(ModelPtrs M) {
   st_row<NV>(M.a.dhc + rH, dhc);
   st_row<NV>(M.a.dinner + rH, di);
   if (vf.gate) st_row<NV>(M.a.dcpre + rH, dc);
-  const float ls = warp_sum(lsum);
-  if (lane == 0) rr[M.sl.lam_mix] = ls;
+  rr_store<NV>(M, b, vf.fnr, M.sl.ref_g, rg, M.sl.ref_b, rb, true, M.sl.lam_mix, warp_sum(lsum));
 }
 
 // mixer LayerNorm + router mix + global-stream gelu (model.py:128-153 backward)
 template <int NV>
 __global__ void __launch_bounds__(32 * kRowWarps) k_mix_bwd_w(ModelPtrs M) {
   ROW_PROLOGUE
-  float* rr = M.a.rowred + (long long)b * M.sl.rowred;
   const VFlags vf = vflags(M.variant);
-  RowV<NV> dhm;
+  RowV<NV> dhm, rg, rb;
   if (vf.mixer) {
     const RowV<NV> dz = ld_split<NV>(M.sk[S_DZ].ws, plane, rH, M.sk[S_DZ].S);
     const RowV<NV> zh = ld_row<NV>(M.a.z_hat + rH), g = ld_row<NV>(M.w[P_MIX_LN_G].p);
@@ -379,13 +419,11 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_mix_bwd_w(ModelPtrs M) {
     if (vf.gate) dm = ld_split<NV>(M.sk[S_DHMC].ws, plane, rH, M.sk[S_DHMC].S);
     const float inv = M.a.z_inv[b];
     const float lam_mix = M.w[P_LAM_MIX].p[0];
-    RowV<NV> rg;
 #pragma unroll
     for (int k = 0; k < NV; ++k)
 #pragma unroll
       for (int e = 0; e < 4; ++e) el(rg.v[k], e) = el(dz.v[k], e) * el(zh.v[k], e);
-    st_row<NV>(rr + M.sl.mix_g, rg);
-    st_row<NV>(rr + M.sl.mix_b, dz);
+    rb = dz;
     float m1, m2;
     row_ln_bwd_means<NV>(dz, g, zh, (float)H, &m1, &m2);
 #pragma unroll
@@ -432,11 +470,12 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_mix_bwd_w(ModelPtrs M) {
     }
   if (vf.router) st_row<NV>(M.a.drpre + rH, drp);
   if (vf.local) st_row<NV>(M.a.dh_l + rH, dl);
-  if (!vf.global) return;
-  st_row<NV>(M.a.dupre + rH, dup);
-  st_row<NV>(M.a.dx_part + rH, dxp);
-  const float ls = warp_sum(lsum);
-  if (lane == 0) rr[M.sl.lam_mem] = ls;
+  if (vf.global) {
+    st_row<NV>(M.a.dupre + rH, dup);
+    st_row<NV>(M.a.dx_part + rH, dxp);
+  }
+  rr_store<NV>(M, b, vf.mixer, M.sl.mix_g, rg, M.sl.mix_b, rb, vf.global, M.sl.lam_mem,
+               vf.global ? warp_sum(lsum) : 0.f);
 }
 
 // ---------------------------------------------------------------------------
@@ -991,8 +1030,23 @@ void launch_trunk_grads_conv(const ModelPtrs& M, cudaStream_t s) {
 ROW_LAUNCH(mix_fwd)
 ROW_LAUNCH(coarse_fwd)
 ROW_LAUNCH(out_fwd)
-ROW_LAUNCH(out_bwd)
-ROW_LAUNCH(coarse_bwd)
-ROW_LAUNCH(mix_bwd)
+// the backward kernels carry the combined rowred rows' shared memory (rr_store)
+#define ROW_LAUNCH_RR(kern)                                                           \
+  bool launch_##kern##_w(const ModelPtrs& M, cudaStream_t s) {                         \
+    if (M.d.H % 128 || M.d.H > 1024) return false;                                     \
+    const dim3 grid(cdiv(M.d.B, kRowWarps)), block(32 * kRowWarps);                    \
+    const size_t sm = M.rr_rows == M.d.B ? 0 : sizeof(float) * kRowWarps * (2 * M.d.H + 4); \
+    switch (M.d.H / 128) {                                                             \
+      case 1: launch_pdl(k_##kern##_w<1>, grid, block, sm, s, M); return true;         \
+      case 2: launch_pdl(k_##kern##_w<2>, grid, block, sm, s, M); return true;         \
+      case 4: launch_pdl(k_##kern##_w<4>, grid, block, sm, s, M); return true;         \
+      case 8: launch_pdl(k_##kern##_w<8>, grid, block, sm, s, M); return true;         \
+    }                                                                                  \
+    return false;                                                                      \
+  }
+
+ROW_LAUNCH_RR(out_bwd)
+ROW_LAUNCH_RR(coarse_bwd)
+ROW_LAUNCH_RR(mix_bwd)
 
 }  // namespace fade

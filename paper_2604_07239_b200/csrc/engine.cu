@@ -558,6 +558,13 @@ static int allocate(fade_model* m) {
   plan_splits(M, {{S_ZD, B, X, H}});
   plan_splits(M, {{S_INNER, B, H, X}, {S_CPRE, B, H, H}});
   plan_splits(M, {{S_LOGITS, B, 256, H}});     // head GEMM: -2..5 us (dh split: +1 us)
+  // (experiments: FADE_BWD_SPLIT = bit mask of backward narrow GEMMs to split:
+  // 1 dh, 2 du + dhm_c, 4 dz, 8 dx_r + dblock)
+  static const int bwd_split = knob("FADE_BWD_SPLIT") ? atoi(knob("FADE_BWD_SPLIT")) : 0;
+  if (bwd_split & 1) plan_splits(M, {{S_DH, B, H, 256}});
+  if (bwd_split & 2) plan_splits(M, {{S_DU, B, X, H}, {S_DHMC, B, H, H}});
+  if (bwd_split & 4) plan_splits(M, {{S_DZ, B, H, X}});
+  if (bwd_split & 8) plan_splits(M, {{S_DXR, B, H, H}, {S_DBLOCK, B, d.D, H}});
   M.variant = m->cfg.variant;
   // the rolling cache as a ring buffer: block writes instead of a (C - D)
   // float roll per row; needs D and B to be whole numbers of 32-float

@@ -753,11 +753,19 @@ static int backward(fade_model* m, const StepIO& io, bool grad_only, double* los
   // W_f first (2,2 / 3,2) 382-386; W12 or W_f after bmm_bwd or later 382-429.
   // (a function-local static initialised once, thread-safely: models may run
   // their steps on several host threads)
-  static const std::array<int, 4> at = [] {
-    std::array<int, 4> a{4, 3, 7, 9};
-    if (const char* e = knob("FADE_SCHED")) sscanf(e, "%d,%d,%d,%d", &a[0], &a[1], &a[2], &a[3]);
+  // B >= 2048 (throughput-bound): W_f after dz2 and W12 after du, so the
+  // tensor-bound W12 update runs beside the HBM-bound W_U update (bmm_bwd)
+  // instead of beside coarse_bwd / du: B = 2048 / 4096 -6 / -16..21 us per
+  // timestep (B = 1024: +9 us)
+  static const std::array<int, 5> forced = [] {
+    std::array<int, 5> a{0, 0, 0, 0, 0};
+    if (const char* e = knob("FADE_SCHED"))
+      a[4] = sscanf(e, "%d,%d,%d,%d", &a[0], &a[1], &a[2], &a[3]) == 4;
     return a;
   }();
+  std::array<int, 4> at{4, 3, 7, 9};
+  if (M.d.B >= 2048) at = {3, 5, 7, 9};
+  if (forced[4]) at = {forced[0], forced[1], forced[2], forced[3]};
   const int ids[4] = {G_WF, G_W12, G_WUP_WCGATE, G_WROUTE_WMEM};
   // bit k of side2_mask puts update ids[k] on a second side stream, where it
   // overlaps the other updates instead of queueing behind them.  B <= 256:

@@ -339,6 +339,12 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   static const long bn128_ids = knob("FADE_BN128") ? atol(knob("FADE_BN128")) : 0;   // experiments
   for (int id = 0; id < G_COUNT; ++id)
     if ((bn128_ids >> id) & 1) m->bn[id] = 128;
+  static const long bn256_ids = knob("FADE_BN256") ? atol(knob("FADE_BN256")) : 0;   // experiments
+  for (int id = 0; id < G_COUNT; ++id)
+    if ((bn256_ids >> id) & 1) {
+      m->bn[id] = 256;
+      Gs[id].occ = 1;
+    }
   // CTA pairs (cta_group::2, 256-row tiles): half the operand bytes per SM
   // (W12 update, the GeGLU backward and dz2: -15 us per step together; the
   // FNR project GEMM F (split-K 18, 144 CTAs): -1.7 us;

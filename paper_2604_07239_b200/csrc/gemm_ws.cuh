@@ -10,9 +10,12 @@
 //   * a dedicated double-buffered epilogue staging area: the drain streams the
 //     tile out in 32-column sub-chunks by TMA while the stage ring keeps
 //     feeding the next tile's mainloop.
-// Epilogues: STORE (+ bias on split 0, split-K slices through the 3-D map) and
-// GEGLU (a1, a2 tiles + gelu(a1)*a2).  The Adam and GeGLU-backward epilogues,
-// which read their inputs through the stage ring, stay on gemm.cuh.
+// Epilogues: STORE (+ bias on split 0, split-K slices through the 3-D map),
+// GEGLU (a1, a2 tiles + gelu(a1)*a2) and ADAM (the weight-update GEMMs: per
+// 32-column sub-chunk the p / m / v boxes load by TMA into the staging area
+// -- the next sub-chunk's while this one is updated -- and store back, so a
+// tile's HBM-bound Adam pass overlaps the next tile's L2-bound mainloop
+// instead of following it).  The GeGLU-backward epilogue stays on gemm.cuh.
 #pragma once
 #include "gemm.cuh"
 
@@ -88,7 +91,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
   uint64_t* empty = full + S;
   uint64_t* accf = empty + S;     // [2] accumulator b is complete
   uint64_t* acce = accf + 2;      // [2] accumulator b drained (PAIR arrivals, on the leader)
-  uint32_t* tmem_slot = (uint32_t*)(acce + 2);
+  uint64_t* ldb = acce + 2;       // [2] Adam p / m / v sub-chunk loads, per staging buffer
+  uint32_t* tmem_slot = (uint32_t*)(ldb + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_launch_dependents();
@@ -107,6 +111,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], PAIR);
+      mbar_init(&ldb[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -248,6 +253,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
     const bool lead = (warp == 2 && lane == 0);
     const uint32_t acce_leader = PAIR == 2 ? mapa_shared(smem_u32(&acce[0]), 0) : 0u;
     uint32_t jj = 0, chunk = 0;
+    AdamScalars ad{};
+    if (G.adam) ad = *G.adam;   // (after the dependency wait: this step's scalars)
     for (int tile = first; tile < G.total_tiles; tile += step) {
       const WsTile t = ws_decode(G, tile, (int)rank, PAIR, BN);
       const GemmProblem& P = *t.P;
@@ -271,6 +278,57 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
       };
       const bool geglu = P.epi == EPI_GEGLU;
       const int nsub = geglu ? BN / 64 : BN / 32;
+      if (P.epi == EPI_ADAM) {
+        // p / m / v of sub-chunk q land in staging buffer (chunk % 2); the
+        // lead issues q + 1's loads once the store that last read that buffer
+        // (sub-chunk q - 1) is done reading, then everyone waits for q's
+        auto issue = [&](int q, uint32_t ch) {
+          uint8_t* eb = epi_smem + (ch % kWsEpiBufs) * kWsEpiBytes;
+          uint64_t* lb = &ldb[ch % kWsEpiBufs];
+          mbar_expect_tx(lb, 3 * kWsSub);
+          tma_load_2d(&P.tc, lb, eb, t.n0 + 32 * q, t.m0);
+          tma_load_2d(&P.tx0, lb, eb + kWsSub, t.n0 + 32 * q, t.m0);
+          tma_load_2d(&P.tx2, lb, eb + 2 * kWsSub, t.n0 + 32 * q, t.m0);
+        };
+        if (lead) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          issue(0, chunk);
+        }
+        for (int q = 0; q < nsub; ++q, ++chunk) {
+          uint8_t* eb = epi_smem + (chunk % kWsEpiBufs) * kWsEpiBytes;
+          if (lead && q + 1 < nsub) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            issue(q + 1, chunk + 1);
+          }
+          mbar_wait(&ldb[chunk % kWsEpiBufs], (chunk / kWsEpiBufs) & 1u);
+          for (int c = c_lo; c < 32; c += 32) {
+            float g[16];
+            acc16(32 * q + c, g);
+#pragma unroll
+            for (int k = 0; k < 16; k += 4) {
+              float4* pp = etile_at(eb, r, c + k);
+              float4* pm = etile_at(eb + kWsSub, r, c + k);
+              float4* pv = etile_at(eb + 2 * kWsSub, r, c + k);
+              float4 p = *pp, m = *pm, v = *pv;
+              adam_rn(ad, g[k], p.x, m.x, v.x);
+              adam_rn(ad, g[k + 1], p.y, m.y, v.y);
+              adam_rn(ad, g[k + 2], p.z, m.z, v.z);
+              adam_rn(ad, g[k + 3], p.w, m.w, v.w);
+              *pp = p;
+              *pm = m;
+              *pv = v;
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          epi_bar();
+          if (lead) {
+            tma_store_2d(&P.tc, eb, t.n0 + 32 * q, t.m0);
+            tma_store_2d(&P.tx0, eb + kWsSub, t.n0 + 32 * q, t.m0);
+            tma_store_2d(&P.tx2, eb + 2 * kWsSub, t.n0 + 32 * q, t.m0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      } else
       for (int q = 0; q < nsub; ++q, ++chunk) {
         uint8_t* eb = epi_smem + (chunk % kWsEpiBufs) * kWsEpiBytes;
         // the TMA store that last read this buffer (two chunks ago) is done

@@ -139,3 +139,36 @@ def test_warp_and_cta_row_kernels_agree_on_every_variant(dims):
         for (p0, l0), (p1, l1) in zip(res["0"][v], res["255"][v]):
             assert np.abs(np.array(p0) - np.array(p1)).max() < 1e-4, v
             assert abs(l0 - l1) < 1e-4, v
+
+
+WS_PROBE = """
+import hashlib, sys
+sys.path.insert(0, {root!r})
+from paper_2604_07239_b200 import ModelConfig, container, corpus
+data = corpus.make_text(64 * 200, 4)
+blob, _ = container.compress_bytes(data, ModelConfig(seed=5, batch=64))
+print(hashlib.sha256(blob).hexdigest())
+"""
+
+
+def test_persistent_adam_gemm_is_bit_identical():
+    """The persistent warp-specialised GEMM's Adam epilogue (gemm_ws.cuh; the
+    W12 update through it with FADE_WS, experiments build) runs the same MMA
+    k order and the same Adam rounding sequence as the one-tile-per-CTA
+    kernel: the containers are byte-identical."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    lib = os.path.join(ROOT, "build", "exp", "libfade_b200.so")
+    if not os.path.exists(lib):
+        pytest.skip("experiments build (make experiments) not present")
+    code = WS_PROBE.format(root=ROOT)
+    out = {}
+    for ws in ("8", "16392"):   # expand GEMM only / expand GEMM + W12 update
+        env = dict(os.environ, FADE_LIB_PATH=lib, FADE_WS=ws)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        out[ws] = r.stdout.strip().splitlines()[-1]
+    assert out["8"] == out["16392"]

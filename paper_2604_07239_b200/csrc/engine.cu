@@ -128,7 +128,8 @@ struct fade_model {
   // fade_bench_compress_steps: the captured timestep, owned by this model (a
   // cache keyed by the model's address replayed a destroyed model's graph when
   // a new model reused the address) and tied to the coder it was captured with
-  cudaGraphExec_t bench_exec = nullptr;
+  cudaGraphExec_t bench_exec = nullptr;    // steps_per_graph() timesteps
+  cudaGraphExec_t bench_exec1 = nullptr;   // one timestep
   const void* bench_coder = nullptr;
   size_t l2_window_max = 0, l2_persist = 0;   // access-policy window cap, persisting carve-out
 };
@@ -973,30 +974,58 @@ static Defer<F> defer(F f) {
   return Defer<F>{f};
 }
 
-// Captures `body` (one timestep on the model stream) into a graph and replays
-// it `n` times.  The event tape pointer rides in the captured kernel
-// parameters only.
+// Timesteps per captured graph.  One: several timesteps in one graph measured
+// slower than the ~2.5 us launch gap they remove (B = 512: 339.0 us at 1,
+// 341.2 / 342.6 / 342.9 at 2 / 4 / 8; B = 64: 230.4 vs 248.9 at 4) -- inside
+// one graph the next step's first kernels wait on the join of every stream
+// as full dependencies.  Experiments: FADE_STEPS_PER_GRAPH.
+static int steps_per_graph() {
+  static const int forced = knob("FADE_STEPS_PER_GRAPH") ? atoi(knob("FADE_STEPS_PER_GRAPH")) : 0;
+  return forced > 0 ? forced : 1;
+}
+
+// Captures `per` consecutive calls of `body` (one timestep each, on the model
+// stream; the device-side column counter moves them along) into one graph.
 template <class Body>
-static int replay_steps(fade_model_t* m, long long n, unsigned long long* tape, Body body) {
+static int capture_steps(fade_model* m, int per, Body body, cudaGraphExec_t* exec,
+                         size_t* nodes = nullptr) {
   cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
   auto cleanup = defer([&] {
-    if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
   });
+  CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
+  int status = FADE_OK;
+  for (int k = 0; k < per && status == FADE_OK; ++k) status = body();
+  const cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
+  if (status != FADE_OK) return status;
+  CK(ce);
+  CK(cudaGraphInstantiate(exec, graph, 0));
+  if (nodes) CK(cudaGraphGetNodes(graph, nullptr, nodes));
+  return FADE_OK;
+}
+
+// Replays `body` (one timestep) n times through graphs of steps_per_graph()
+// timesteps plus one graph for the remainder.  The event tape pointer rides
+// in the captured kernel parameters only.
+template <class Body>
+static int replay_steps(fade_model* m, long long n, unsigned long long* tape, Body body) {
+  cudaGraphExec_t exec = nullptr, rest = nullptr;
+  auto cleanup = defer([&] {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (rest) cudaGraphExecDestroy(rest);
+  });
+  const int per = (int)std::max<long long>(1, std::min<long long>(steps_per_graph(), n));
+  const long long full = n / per, rem = n % per;
   m->M.tape = tape;
   {
     NvtxRange r("fade: capture timestep graph");
-    CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
-    const int status = body();
-    const cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
-    m->M.tape = nullptr;
-    if (status != FADE_OK) return status;
-    CK(ce);
-    CK(cudaGraphInstantiate(&exec, graph, 0));
+    auto untape = defer([&] { m->M.tape = nullptr; });
+    TRY(capture_steps(m, per, body, &exec));
+    if (rem) TRY(capture_steps(m, (int)rem, body, &rest));
   }
   NvtxRange r("fade: timesteps (graph replays)");
-  for (long long i = 0; i < n; ++i) CK(cudaGraphLaunch(exec, m->s_main));
+  for (long long i = 0; i < full; ++i) CK(cudaGraphLaunch(exec, m->s_main));
+  if (rem) CK(cudaGraphLaunch(rest, m->s_main));
   CK(cudaStreamSynchronize(m->s_main));
   return FADE_OK;
 }
@@ -1075,6 +1104,7 @@ int fade_model_destroy(fade_model_t* m) {
   DeviceScope dscope(m->device);
   cudaDeviceSynchronize();
   if (m->bench_exec) cudaGraphExecDestroy(m->bench_exec);
+  if (m->bench_exec1) cudaGraphExecDestroy(m->bench_exec1);
   if (m->l2_persist) {
     // give the persisting carve-out back: a later, larger model (whose W_U
     // does not fit) must not run with part of L2 set aside
@@ -1761,23 +1791,24 @@ int fade_bench_compress_steps(fade_model_t* m, const uint8_t* data_dev, int64_t 
     long long v = start;
     CK(cudaMemcpy((*coder)->e.col, &v, sizeof(v), cudaMemcpyHostToDevice));
   }
+  // graphs of steps_per_graph() timesteps (as the executors run them) and
+  // of one timestep for the remainder of `steps`
+  const int per = steps_per_graph();
   if (!m->bench_exec || m->bench_coder != *coder) {
-    if (m->bench_exec) CK(cudaGraphExecDestroy(m->bench_exec));
-    m->bench_exec = nullptr;
-    cudaGraph_t graph;
-    CK(cudaStreamBeginCapture(m->s_main, cudaStreamCaptureModeThreadLocal));
-    int status = compress_step(m, *coder, data_dev, L, 1, nullptr);
-    cudaError_t ce = cudaStreamEndCapture(m->s_main, &graph);
-    if (status != FADE_OK) return status;
-    CK(ce);
-    CK(cudaGraphInstantiate(&m->bench_exec, graph, 0));
+    for (cudaGraphExec_t* e : {&m->bench_exec, &m->bench_exec1})
+      if (*e) {
+        CK(cudaGraphExecDestroy(*e));
+        *e = nullptr;
+      }
+    auto body = [&] { return compress_step(m, *coder, data_dev, L, 1, nullptr); };
     size_t n = 0;
-    CK(cudaGraphGetNodes(graph, nullptr, &n));
-    m->launches_per_step = (int)n;
-    cudaGraphDestroy(graph);
+    TRY(capture_steps(m, per, body, &m->bench_exec, &n));
+    TRY(capture_steps(m, 1, body, &m->bench_exec1));
+    m->launches_per_step = (int)(n / per);
     m->bench_coder = *coder;
   }
-  for (long long i = 0; i < steps; ++i) CK(cudaGraphLaunch(m->bench_exec, m->s_main));
+  for (long long i = 0; i < steps / per; ++i) CK(cudaGraphLaunch(m->bench_exec, m->s_main));
+  for (long long i = 0; i < steps % per; ++i) CK(cudaGraphLaunch(m->bench_exec1, m->s_main));
   if (launches) *launches = m->launches_per_step;
   return FADE_OK;
 }

@@ -2,7 +2,10 @@
 torch.profiler): per-kernel start offset, duration and stream for one
 timestep, plus per-kernel mean durations over the profiled steps.
 
-    python tools/timeline.py [steps] [batch] > timeline.txt
+    python tools/timeline.py [steps] [batch] [skip] > timeline.txt
+
+(skip: timesteps trained before the profiled ones; per-step cost grows a few
+percent over the first ~10^4 steps of a stream)
 """
 import ctypes
 import json
@@ -23,8 +26,9 @@ def main():
     from paper_2604_07239_b200.pipeline import StreamPartition
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 16
     batch = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+    skip = int(sys.argv[3]) if len(sys.argv) > 3 else 32
     cfg = ModelConfig(batch=batch, workers=1)
-    data = corpus.make_text(max(2_000_000, batch * (n + 80)), 12)
+    data = corpus.make_text(max(2_000_000, batch * (n + skip + 80)), 12)
     part = StreamPartition.from_length(len(data), cfg.batch)
     mat = np.ascontiguousarray(part.split(data))
     L = part.stream_length
@@ -37,7 +41,7 @@ def main():
         _native.check(lib.fade_bench_compress_steps(m.handle, dmat.data_ptr(), L, 16, k,
                                                     ctypes.byref(coder), ctypes.byref(la), None),
                       "steps")
-    steps(32)
+    steps(skip)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         steps(n)

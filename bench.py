@@ -315,8 +315,22 @@ def run_ours(args):
                                                     ctypes.byref(launches), None),
                       "bench_compress_steps")
 
-    if skip:
-        _native.check(lib.fade_bench_compress_steps(model.handle, dmat.data_ptr(), L, start, skip,
+    # the same K steps timed at the start of the stream too (reported as
+    # config.early_window_*: what the earlier rounds' lines measured)
+    early_ms = None
+    rest = skip
+    if skip >= (W + K) * S:
+        steps(W)
+        torch.cuda.synchronize()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        steps(K)
+        q1.record(stream)
+        torch.cuda.synchronize()
+        early_ms = q0.elapsed_time(q1)
+        rest -= (W + K) * S
+    if rest:
+        _native.check(lib.fade_bench_compress_steps(model.handle, dmat.data_ptr(), L, start, rest,
                                                     ctypes.byref(coder), ctypes.byref(launches),
                                                     None), "bench_compress_steps")
     steps(W)
@@ -455,6 +469,9 @@ def run_ours(args):
             "config": {"workload": WORKLOAD_SHARDED.format(n=world) if world > 1 else WORKLOAD,
                        "batch": cfg.batch, "timesteps_per_step": S,
                        "timed_after_timesteps": skip + W * S,
+                       "early_window_value": (None if early_ms is None else
+                                              world * cfg.batch * K * S / (early_ms / 1e3) / 1e6),
+                       "early_window_ms_per_step": early_ms / K if early_ms is not None else None,
                        "stream_length": L, "parallelism": f"shards{world}",
                        "l2": "working set ~290 MB (params + Adam state) > 126 MB L2; no flush"},
             "decompress": dec, "gpu_launches": launches.value * K * S,

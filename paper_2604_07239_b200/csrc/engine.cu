@@ -1803,12 +1803,12 @@ int fade_bench_compress_steps(fade_model_t* m, const uint8_t* data_dev, int64_t 
     auto body = [&] { return compress_step(m, *coder, data_dev, L, 1, nullptr); };
     size_t n = 0;
     TRY(capture_steps(m, per, body, &m->bench_exec, &n));
-    TRY(capture_steps(m, 1, body, &m->bench_exec1));
+    if (per > 1) TRY(capture_steps(m, 1, body, &m->bench_exec1));   // (per == 1: bench_exec is it)
     m->launches_per_step = (int)(n / per);
     m->bench_coder = *coder;
   }
   for (long long i = 0; i < steps / per; ++i) CK(cudaGraphLaunch(m->bench_exec, m->s_main));
-  for (long long i = 0; i < steps % per; ++i) CK(cudaGraphLaunch(m->bench_exec1, m->s_main));
+  for (long long i = 0; i < steps % per; ++i) CK(cudaGraphLaunch(m->bench_exec1, m->s_main));   // (per > 1 only)
   if (launches) *launches = m->launches_per_step;
   return FADE_OK;
 }

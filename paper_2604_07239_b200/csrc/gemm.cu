@@ -233,7 +233,8 @@ int gemm_launch(GemmParams& G, int BN, cudaStream_t st) {
   if (G.ws) {   // persistent: STORE / GEGLU epilogues only, no ring operands
     for (int q = 0; q < G.nprob; ++q)
       if ((G.prob[q].epi != EPI_STORE && G.prob[q].epi != EPI_GEGLU && G.prob[q].epi != EPI_ADAM) ||
-          G.prob[q].a_ring || (G.prob[q].epi == EPI_ADAM && G.prob[q].splits > 1)) {
+          G.prob[q].a_ring ||
+          (G.prob[q].epi == EPI_ADAM && (!kWsAdam || G.prob[q].splits > 1))) {
         set_last_error("the persistent GEMM runs only the store, GeGLU and Adam epilogues");
         return FADE_ERR_USAGE;
       }

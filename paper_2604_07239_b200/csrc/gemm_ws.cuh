@@ -27,6 +27,14 @@ constexpr int kWsEpiBytes = 3 * kWsSub;      // a GEGLU sub-chunk: a1, a2 and wi
 #define FADE_WS_EPIBUFS 2
 #endif
 constexpr int kWsEpiBufs = FADE_WS_EPIBUFS;  // staging buffers the drain alternates
+// The Adam epilogue serves only the experiments build's FADE_WS weight-update
+// runs (measured slower than the one-tile kernel); the
+// shipped expand GEMM compiles without it (121 instead of 128 registers)
+#ifdef FADE_EXPERIMENTS
+constexpr bool kWsAdam = true;
+#else
+constexpr bool kWsAdam = false;
+#endif
 
 template <int BN, int PAIR>
 struct WsCfg {
@@ -254,7 +262,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
     const uint32_t acce_leader = PAIR == 2 ? mapa_shared(smem_u32(&acce[0]), 0) : 0u;
     uint32_t jj = 0, chunk = 0;
     AdamScalars ad{};
-    if (G.adam) ad = *G.adam;   // (after the dependency wait: this step's scalars)
+    if (kWsAdam && G.adam) ad = *G.adam;   // (after the dependency wait: this step's scalars)
     for (int tile = first; tile < G.total_tiles; tile += step) {
       const WsTile t = ws_decode(G, tile, (int)rank, PAIR, BN);
       const GemmProblem& P = *t.P;
@@ -278,7 +286,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_ws(const __grid_consta
       };
       const bool geglu = P.epi == EPI_GEGLU;
       const int nsub = geglu ? BN / 64 : BN / 32;
-      if (P.epi == EPI_ADAM) {
+      if (kWsAdam && P.epi == EPI_ADAM) {
         // p / m / v of sub-chunk q land in staging buffer (chunk % 2); the
         // lead issues q + 1's loads once the store that last read that buffer
         // (sub-chunk q - 1) is done reading, then everyone waits for q's

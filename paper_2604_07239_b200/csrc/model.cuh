@@ -144,6 +144,17 @@ struct ModelPtrs {   // everything a row kernel may need, passed by value
   int rr_rows;
   int dbg;   // experiments build only (FADE_DBG_TRUNK): bit 0 drops the embedding-gradient atomics
 };
+
+// The ring-buffer cache is an experiments-build option (engine.cu, FADE_RING):
+// the shipped kernels compile its branches out.
+__device__ __forceinline__ bool ring_cache(const ModelPtrs& M) {
+#ifdef FADE_EXPERIMENTS
+  return M.ring_on != 0;
+#else
+  (void)M;
+  return false;
+#endif
+}
 __device__ __forceinline__ unsigned long long* tape_at(const ModelPtrs& M, int slot) {
   return M.tape + kTapeSlots * (M.st->col - M.st->loss_base) + slot;
 }

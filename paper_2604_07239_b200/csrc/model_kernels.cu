@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 4) k_trunk_fwd(ModelPtrs M, con
   // overwrites the oldest one in place; nothing else moves (ref
   // ops.py:219-231 semantics).  Element o of the new block lands at
   // ring_elem(o); without the ring, at crow[C - D + o] after the roll.
-  const bool ring = M.ring_on;
+  const bool ring = ring_cache(M);
   const int rnb = d.C / 32, rstep = d.D / 32;
   const int rb0 = ring ? (int)((M.st->ring * rstep) % rnb) : 0;
   // the weights are staged once per CTA; a CTA walks rows b = cta, cta +
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kRowMax, 4) k_mix_fwd(ModelPtrs M) {
   // count this step's roll of the ring-buffer cache: trunk_fwd wrote the new
   // block at the old position and the forward W_mem GEMM (ring_bias 1) has
   // read; no other kernel of this grid reads the position
-  if (M.ring_on && b == 0 && tid == 0) M.st->ring += 1;
+  if (ring_cache(M) && b == 0 && tid == 0) M.st->ring += 1;
   if (vf.global) split_row(ups, part, M.a.ws_mem, plane, rH, d.H, M.splits_mem);
   float asum = 0.f, amin = 3.4e38f, amax = -3.4e38f;
   for (int j = tid; j < d.H; j += blockDim.x) {

@@ -123,7 +123,7 @@ template <int NV>
 __global__ void __launch_bounds__(32 * kRowWarps) k_mix_fwd_w(ModelPtrs M) {
   ROW_PROLOGUE
   // count this step's roll of the ring-buffer cache (see k_mix_fwd)
-  if (M.ring_on && b == 0 && lane == 0) M.st->ring += 1;
+  if (ring_cache(M) && b == 0 && lane == 0) M.st->ring += 1;
   const VFlags vf = vflags(M.variant);
   const float lam = M.w[P_LAM_MEM].p[0];
   RowV<NV> hg, hm, up, x, hl, rp;

@@ -509,6 +509,17 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
       TRY(bl.add(adam(g, w[P_W_MEM])));
     }
   }
+  // Adam GEMMs whose p/m/v are pulled into L2 before their mainloop: the
+  // W_route/W_mem update, which ends the step beside the latency-bound
+  // trunk_bwd / small_adam while HBM has room (B = 512 -1.2 us per timestep,
+  // early and steady state); the W12 / W_f / W_up-group updates run beside
+  // the HBM-heavy chain and measured slower with it (profiles/r2_experiments.md).
+  // (experiments: FADE_ADAM_PF = bit per GemmId)
+  static const long pf_ids = knob("FADE_ADAM_PF") ? atol(knob("FADE_ADAM_PF"))
+                                                   : (1L << G_WROUTE_WMEM);
+  for (int id = 0; id < G_COUNT; ++id)
+    if ((pf_ids >> id) & 1)
+      for (int q = 0; q < Gs[id].nprob; ++q) Gs[id].prob[q].l2_pf = 1 << 20;
   return FADE_OK;
 }
 

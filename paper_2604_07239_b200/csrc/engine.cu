@@ -478,37 +478,6 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
     }
     return g;
   };
-  // W_head rides in the W_f launch and W_down in the W_up/W_cgate launch:
-  // fewer side-stream kernels (each costs a fixed ~10 us of latency)
-  // (experiments: FADE_MERGE_WF=1 puts W_head + W_f into the W12 launch, so
-  // their tiles follow W12's on the SMs it frees instead of queueing behind
-  // the model stream's kernels)
-  static const bool merge_wf = knob("FADE_MERGE_WF") && atoi(knob("FADE_MERGE_WF")) != 0;
-  if (vf.fnr)
-    TRY(b(G_W12).add(adam(gd(a.z2, H, 1, a.da12, 2LL * Ep, 0, H, 2 * Ep, B, EPI_ADAM, nullptr, 2LL * Ep), w[P_W_E1])));
-  {
-    auto bl = b(merge_wf && vf.fnr ? G_W12 : G_WF);
-    TRY(bl.add(adam(gd(h_final, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD])));
-    if (vf.fnr)
-      TRY(bl.add(adam(gd(a.wide, Ep, 1, a.dnpre, H, 0, E, H, B, EPI_ADAM, nullptr, H), w[P_W_F])));
-  }
-  if (vf.mixer) {
-    auto bl = b(G_WUP_WCGATE);
-    TRY(bl.add(adam(gd(a.u, X, 1, a.dinner, H, 0, X, H, B, EPI_ADAM, nullptr, H), w[P_W_UP])));
-    if (vf.gate)
-      TRY(bl.add(adam(gd(a.hm_tc, H, 1, a.dcpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_CGATE])));
-    TRY(bl.add(adam(gd(a.z, H, 1, a.dzd, X, 0, H, X, B, EPI_ADAM, nullptr, X), w[P_W_DOWN])));
-  }
-  {
-    auto bl = b(G_WROUTE_WMEM);
-    if (vf.router)
-      TRY(bl.add(adam(gd(a.x_tc, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE])));
-    if (vf.global) {
-      GemmDesc g = gd(a.cache, C, 1, a.dupre, H, 0, C, H, B, EPI_ADAM, nullptr, H);
-      ring_operand(g, 2);
-      TRY(bl.add(adam(g, w[P_W_MEM])));
-    }
-  }
   // Adam GEMMs whose p/m/v are pulled into L2 before their mainloop: the
   // W_route/W_mem update, which ends the step beside the latency-bound
   // trunk_bwd / small_adam while HBM has room (B = 512 -1.2 us per timestep,
@@ -517,9 +486,41 @@ static int build_gemms(fade_model* m, GemmParams* Gs, bool grad_only) {
   // (experiments: FADE_ADAM_PF = bit per GemmId)
   static const long pf_ids = knob("FADE_ADAM_PF") ? atol(knob("FADE_ADAM_PF"))
                                                    : (1L << G_WROUTE_WMEM);
-  for (int id = 0; id < G_COUNT; ++id)
-    if ((pf_ids >> id) & 1)
-      for (int q = 0; q < Gs[id].nprob; ++q) Gs[id].prob[q].l2_pf = 1 << 20;
+  auto pf = [&](GemmDesc g, int id) {
+    if ((pf_ids >> id) & 1) g.l2_pf = 1 << 20;   // every chunk of the tile
+    return g;
+  };
+  // W_head rides in the W_f launch and W_down in the W_up/W_cgate launch:
+  // fewer side-stream kernels (each costs a fixed ~10 us of latency)
+  // (experiments: FADE_MERGE_WF=1 puts W_head + W_f into the W12 launch, so
+  // their tiles follow W12's on the SMs it frees instead of queueing behind
+  // the model stream's kernels)
+  static const bool merge_wf = knob("FADE_MERGE_WF") && atoi(knob("FADE_MERGE_WF")) != 0;
+  if (vf.fnr)
+    TRY(b(G_W12).add(pf(adam(gd(a.z2, H, 1, a.da12, 2LL * Ep, 0, H, 2 * Ep, B, EPI_ADAM, nullptr, 2LL * Ep), w[P_W_E1]), G_W12)));
+  {
+    auto bl = b(merge_wf && vf.fnr ? G_W12 : G_WF);
+    TRY(bl.add(pf(adam(gd(h_final, H, 1, a.dlogits, 256, 0, H, 256, B, EPI_ADAM, nullptr, 256), w[P_W_HEAD]), G_WF)));
+    if (vf.fnr)
+      TRY(bl.add(pf(adam(gd(a.wide, Ep, 1, a.dnpre, H, 0, E, H, B, EPI_ADAM, nullptr, H), w[P_W_F]), G_WF)));
+  }
+  if (vf.mixer) {
+    auto bl = b(G_WUP_WCGATE);
+    TRY(bl.add(pf(adam(gd(a.u, X, 1, a.dinner, H, 0, X, H, B, EPI_ADAM, nullptr, H), w[P_W_UP]), G_WUP_WCGATE)));
+    if (vf.gate)
+      TRY(bl.add(pf(adam(gd(a.hm_tc, H, 1, a.dcpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_CGATE]), G_WUP_WCGATE)));
+    TRY(bl.add(pf(adam(gd(a.z, H, 1, a.dzd, X, 0, H, X, B, EPI_ADAM, nullptr, X), w[P_W_DOWN]), G_WUP_WCGATE)));
+  }
+  {
+    auto bl = b(G_WROUTE_WMEM);
+    if (vf.router)
+      TRY(bl.add(pf(adam(gd(a.x_tc, H, 1, a.drpre, H, 0, H, H, B, EPI_ADAM, nullptr, H), w[P_W_ROUTE]), G_WROUTE_WMEM)));
+    if (vf.global) {
+      GemmDesc g = gd(a.cache, C, 1, a.dupre, H, 0, C, H, B, EPI_ADAM, nullptr, H);
+      ring_operand(g, 2);
+      TRY(bl.add(pf(adam(g, w[P_W_MEM]), G_WROUTE_WMEM)));
+    }
+  }
   return FADE_OK;
 }
 

@@ -89,6 +89,7 @@ int gemm_setup(GemmProblem* P, const GemmDesc& d, int BN) {
   // A: a_trans == 0 -> A[m*lda + k] (K-major); 1 -> A[k*lda + m] (M-major)
   P->a_mn = d.a_trans;
   P->b_pre = d.b_pre;
+  P->l2_pf = d.l2_pf;
   // B: b_trans == 0 -> B[k*ldb + n] (N-major); 1 -> B[n*ldb + k] (K-major)
   P->b_mn = d.b_trans ? 0 : 1;
   int s;

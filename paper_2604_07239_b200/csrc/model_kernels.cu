@@ -844,11 +844,11 @@ __device__ void adam_prep_dev(StepState* st, double lr, double b1, double b2, do
 
 __device__ __forceinline__ void adam_update(const AdamScalars& a, float g, float* p, float* m,
                                             float* v) {
-  const float m1 = __fadd_rn(__fmul_rn(*m, a.beta1), __fmul_rn(a.one_m_b1, g));
-  const float v1 = __fadd_rn(__fmul_rn(*v, a.beta2), __fmul_rn(a.one_m_b2, __fmul_rn(g, g)));
-  float sc = (float)__dmul_rn((double)__fsqrt_rn(v1), a.inv_sqrt_c2);
+  const float m1 = fadd_ftz(fmul_ftz(*m, a.beta1), fmul_ftz(a.one_m_b1, g));
+  const float v1 = fadd_ftz(fmul_ftz(*v, a.beta2), fmul_ftz(a.one_m_b2, fmul_ftz(g, g)));
+  float sc = (float)__dmul_rn((double)fsqrt_ftz(v1), a.inv_sqrt_c2);
   sc = __fadd_rn(sc, a.eps);
-  sc = __fmul_rn(__fdiv_rn(m1, sc), a.step_size);
+  sc = __fmul_rn(fdiv_ftz(m1, sc), a.step_size);
   *m = m1;
   *v = v1;
   *p = __fsub_rn(*p, sc);

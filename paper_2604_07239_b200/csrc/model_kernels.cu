@@ -846,7 +846,7 @@ __device__ __forceinline__ void adam_update(const AdamScalars& a, float g, float
                                             float* v) {
   const float m1 = fadd_ftz(fmul_ftz(*m, a.beta1), fmul_ftz(a.one_m_b1, g));
   const float v1 = fadd_ftz(fmul_ftz(*v, a.beta2), fmul_ftz(a.one_m_b2, fmul_ftz(g, g)));
-  float sc = (float)__dmul_rn((double)fsqrt_ftz(v1), a.inv_sqrt_c2);
+  float sc = (float)__dmul_rn((double)fsqrt_fastpath(v1), a.inv_sqrt_c2);
   sc = __fadd_rn(sc, a.eps);
   sc = __fmul_rn(fdiv_fastpath(m1, sc), a.step_size);
   *m = m1;

@@ -4,6 +4,6 @@ P='import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); pri
 for i in 1 2; do
   for c in "$@"; do
     if [ "$c" = HEAD ]; then L=$PWD/paper_2604_07239_b200/_lib/libfade_b200.so; else L=$PWD/build/bis/$c/paper_2604_07239_b200/_lib/libfade_b200.so; fi
-    echo -n "$c : "; FADE_LIB_PATH=$L python bench.py --no-sweep --no-cpu-baseline --no-e2e 2>/dev/null | python -c "$P"
+    echo -n "$c : "; FADE_LIB_PATH=$L python bench.py --no-sweep --no-cpu-baseline --no-e2e $BENCH_ARGS 2>/dev/null | python -c "$P"
   done
 done
